@@ -1,0 +1,108 @@
+/*
+ * lfbp_hprime.h -- C ABI of the B200-native H -> H' rearrangement.
+ *
+ * Drop-in boundary for the reference's hot path, the pure-Python `lfbp`
+ * package (arXiv 2003.09133).  Arrays are the reference's layout: 5-D
+ * (n_s, n_t, n_x, n_y, n_z), Fortran order (s fastest, z slowest; reference
+ * arrays.py:21-23, fileio.py:13), element type float32 or float64 moved
+ * bit-exactly.  Every entry point takes plain pointers and sizes; no torch
+ * or CUDA types appear in the signatures (streams are passed as void*,
+ * a cudaStream_t / CUstream, NULL = legacy default stream).
+ *
+ * Which reference interface each entry point replaces:
+ *   lfbp_hprime_device / lfbp_hprime_host
+ *       -> lfbp.compute_backprojection(psf)            transform.py:113-135
+ *          (inverse = 1) lfbp.compute_psf_from_backprojection(bp)
+ *                                                    transform.py:138-155
+ *   lfbp_hprime_multi
+ *       -> the same, z-sharded over several GPUs; the reference permits
+ *          parallelism over z-planes but runs one thread
+ *   lfbp_check_dims        -> Dims5 validation        arrays.py:53-67
+ *   lfbp_dropped_source_count -> dropped_source_count transform.py:106-110
+ *   lfbp_compare_device    -> the bitwise np.array_equal verification of
+ *                             bench.py:88 / cli.py:145-150, on the device
+ * Error codes mirror the reference's exceptions (errors.py:12-13, 32-33).
+ */
+#ifndef LFBP_HPRIME_H
+#define LFBP_HPRIME_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define LFBP_OK 0
+#define LFBP_ERR_INVALID_DIMS 1     /* lfbp.InvalidDims   (errors.py:12-13) */
+#define LFBP_ERR_EVEN_PIXEL_DIMS 2  /* lfbp.EvenPixelDims (errors.py:32-33) */
+#define LFBP_ERR_CUDA 3             /* CUDA runtime failure; see lfbp_last_error() */
+#define LFBP_ERR_ARGUMENT 4         /* null / misaligned pointer, bad dtype or range */
+#define LFBP_ERR_UNSUPPORTED 5      /* shape beyond the kernel's limits */
+
+/* element type codes: the LF5 header codes (fileio.py:35) */
+#define LFBP_F32 1
+#define LFBP_F64 2
+
+/* flags for lfbp_hprime_host / lfbp_hprime_multi */
+#define LFBP_HOST_REGISTER 1   /* pin pageable host buffers for the call (cudaHostRegister) */
+
+/* Validate (n_s, n_t, n_x, n_y, n_z) like Dims5 (arrays.py:53-67).
+ * Returns LFBP_OK or LFBP_ERR_INVALID_DIMS. No GPU needed. */
+int lfbp_check_dims(const int64_t dims[5]);
+
+/* Source elements without a target for even n_s / n_t (transform.py:106-110).
+ * Returns -1 for invalid dims. No GPU needed. */
+int64_t lfbp_dropped_source_count(const int64_t dims[5]);
+
+/* H' = rearrange(H) (inverse = 0) or H = rearrange^-1(H') (inverse = 1, odd
+ * n_s and n_t only; otherwise LFBP_ERR_EVEN_PIXEL_DIMS) for depth planes
+ * [z_begin, z_end) of device arrays `src` and `dst` that both hold the WHOLE
+ * (n_s, n_t, n_x, n_y, n_z) array, 16-byte aligned, non-overlapping.
+ * Asynchronous on `stream`; the caller synchronises. */
+int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse,
+                       int64_t z_begin, int64_t z_end, void* stream);
+
+/* Host-to-host H' on one GPU: the z-planes are streamed through the device in
+ * chunks (H2D, kernel and D2H overlapped on three streams).  `src` and `dst`
+ * are host arrays of the whole shape; pinned memory gives full PCIe speed,
+ * pageable memory is pinned for the call when flags has LFBP_HOST_REGISTER.
+ * Synchronous: returns when dst is complete. */
+int lfbp_hprime_host(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse,
+                     int device, int flags);
+
+/* Host-to-host H' with the z-planes split into contiguous slabs, one per
+ * listed device, all devices running concurrently; no inter-GPU traffic.
+ * Each slab lands at its own byte offset z0 * plane_bytes of dst. */
+int lfbp_hprime_multi(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse,
+                      int n_devices, const int* devices, int flags);
+
+/* Contiguous balanced split of n_z planes over n_shards: shard k gets
+ * [*z_begin, *z_end). No GPU needed. */
+int lfbp_shard_planes(int64_t n_z, int n_shards, int shard, int64_t* z_begin, int64_t* z_end);
+
+/* Bitwise comparison of two device buffers of `nbytes` (K2).  Writes the
+ * number of differing bytes and the first differing byte offset (-1 when
+ * equal).  Synchronous. */
+int lfbp_compare_device(const void* a, const void* b, int64_t nbytes, int64_t* n_diff,
+                        int64_t* first_diff, void* stream);
+
+/* The launch plan the kernel would use, as a JSON object in `buf` (for
+ * tests, tuning and DESIGN.md).  Uses the current device's properties, or
+ * B200 defaults (148 SMs, 227 KB smem/CTA) when no GPU is present. */
+int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len);
+
+/* Kernel launches issued by this library since load (all entry points). */
+int64_t lfbp_launch_count(void);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* lfbp_last_error(void);
+
+/* Library version string. */
+const char* lfbp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFBP_HPRIME_H */

@@ -1,0 +1,21 @@
+"""B200-native H -> H' rearrangement (arXiv 2003.09133), drop-in for the
+reference ``lfbp`` hot path.
+
+Public API mirrors ``lfbp/__init__.py:21-23`` for the path:
+``compute_backprojection``, ``compute_psf_from_backprojection``,
+``dropped_source_count``, the ``Dims5`` / ``PsfArray`` / ``BackprojArray``
+types and the ``InvalidDims`` / ``EvenPixelDims`` errors; plus the device
+API ``hprime_device`` and the z-slab launcher in ``shard``.
+"""
+from .arrays import BackprojArray, Dims5, PsfArray
+from .errors import EvenPixelDims, InvalidDims, LfbpError, NativeError, VerificationFailure
+from .transform import (compute_backprojection, compute_psf_from_backprojection, dropped_source_count,
+                        f_order_empty, hprime_device, plan)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BackprojArray", "Dims5", "PsfArray", "EvenPixelDims", "InvalidDims", "LfbpError", "NativeError",
+    "VerificationFailure", "compute_backprojection", "compute_psf_from_backprojection",
+    "dropped_source_count", "f_order_empty", "hprime_device", "plan",
+]

@@ -1,0 +1,530 @@
+// C-ABI of the B200-native H -> H' rearrangement (see include/lfbp_hprime.h).
+//
+// Host runtime around the K1 kernel: dims validation with the reference's
+// rules, the launch planner (work-unit shape, smem ring, persistent grid),
+// device-array entry point, a chunked H2D / kernel / D2H pipeline for host
+// arrays, the z-slab multi-GPU launcher, and the K2 device comparator.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/lfbp_hprime.h"
+#include "hprime_kernel.cuh"
+#include "hprime_plan.h"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define HP_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(LFBP_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),       \
+                  __FILE__, __LINE__);                                                         \
+  } while (0)
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return atoi(v);
+}
+
+struct DevProps {
+  int sm_count = 148;
+  int smem_optin = 232448;  // 227 KB
+  int max_threads_sm = 2048;
+  bool real = false;
+};
+
+std::mutex g_props_mu;
+std::map<int, DevProps> g_props;
+
+DevProps device_props(int dev) {
+  std::lock_guard<std::mutex> lk(g_props_mu);
+  auto it = g_props.find(dev);
+  if (it != g_props.end()) return it->second;
+  DevProps p;
+  int n = 0;
+  if (dev >= 0 && cudaGetDeviceCount(&n) == cudaSuccess && dev < n) {
+    cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&p.max_threads_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+    p.real = true;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(dev);
+    cudaFuncSetAttribute(hp::hprime_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
+    cudaFuncSetAttribute(hp::hprime_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
+    cudaSetDevice(cur);
+  } else {
+    cudaGetLastError();  // clear "no device" state
+  }
+  g_props[dev] = p;
+  return p;
+}
+
+int elem_size(int dtype) { return dtype == LFBP_F32 ? 4 : dtype == LFBP_F64 ? 8 : 0; }
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// Work-unit shape, smem ring and persistent grid for one launch.
+int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_count,
+              int64_t total_bytes, int dev) {
+  memset(&p, 0, sizeof(p));
+  const DevProps dp = device_props(dev);
+  p.n_s = d[0];
+  p.n_t = d[1];
+  p.n_x = d[2];
+  p.n_y = d[3];
+  p.z_begin = z_begin;
+  p.z_count = z_count;
+  p.total_bytes = total_bytes;
+  p.elem = E;
+  p.c_s = static_cast<int32_t>((d[0] - 1) / 2);
+  p.c_t = static_cast<int32_t>((d[1] - 1) / 2);
+  p.v_s = 2 * p.c_s + 1;
+  p.v_t = 2 * p.c_t + 1;
+  p.nx_off = static_cast<int32_t>((d[2] - (p.c_s % d[2])) % d[2]);
+  p.ny_off = static_cast<int32_t>((d[3] - (p.c_t % d[3])) % d[3]);
+  p.xs16 = static_cast<int32_t>((d[0] * d[1] * E) & 15);
+  if (d[0] >= (1ll << 30) || d[1] >= (1ll << 30) || d[2] >= (1 << 20) || d[3] >= (1 << 20))
+    return fail(LFBP_ERR_UNSUPPORTED, "axis too long for the kernel's 32-bit in-plane indices");
+
+  const int64_t stage_target = int64_t(env_int("LFBP_STAGE_KB", 32)) * 1024;
+  const int64_t stage_max = int64_t(env_int("LFBP_STAGE_MAX_KB", 100)) * 1024;
+  const int64_t row_full = d[0] * E;
+  int64_t run_max;
+  if (d[2] * (row_full + 32) <= stage_max) {
+    int64_t J = stage_target / (d[2] * row_full);
+    J = std::max<int64_t>(1, std::min<int64_t>(J, d[1]));
+    const int jcap = env_int("LFBP_BAND", 0);
+    if (jcap > 0) J = std::min<int64_t>(J, jcap);
+    p.J = static_cast<int32_t>(J);
+    p.C = static_cast<int32_t>(d[0]);
+    p.n_chunks = 1;
+    run_max = J * row_full;
+  } else {
+    const int64_t C = (stage_max / d[2] - 32) / E;
+    if (C < 1) return fail(LFBP_ERR_UNSUPPORTED, "n_x=%lld too large to stage one column", (long long)d[2]);
+    p.J = 1;
+    p.C = static_cast<int32_t>(std::min<int64_t>(C, d[0]));
+    p.n_chunks = static_cast<int32_t>((d[0] + p.C - 1) / p.C);
+    run_max = int64_t(p.C) * E;
+  }
+  p.n_bands = static_cast<int32_t>((d[1] + p.J - 1) / p.J);
+  int64_t pitch = round_up(run_max + 32, 16);
+  if (((pitch / 16) & 1) == 0) pitch += 16;  // odd multiple of 16 B spreads rows over banks
+  p.row_pitch = static_cast<int32_t>(pitch);
+  p.stage_bytes = static_cast<int32_t>(round_up(d[2] * pitch, 128));
+  int S = env_int("LFBP_STAGES", 3);
+  S = std::max(1, std::min(S, 8));
+  while (S > 1 && 128 + int64_t(S) * p.stage_bytes > dp.smem_optin) --S;
+  if (128 + int64_t(S) * p.stage_bytes > dp.smem_optin)
+    return fail(LFBP_ERR_UNSUPPORTED, "stage of %d bytes exceeds shared memory", p.stage_bytes);
+  p.stages = S;
+  p.smem_bytes = 128 + S * p.stage_bytes;
+  int threads = env_int("LFBP_THREADS", 0);
+  if (threads <= 0) threads = p.smem_bytes > dp.smem_optin / 2 ? 512 : 256;
+  threads = std::max(32, std::min(512, threads / 32 * 32));
+  p.threads = threads;
+
+  const int64_t units = z_count * p.n_chunks * int64_t(p.n_bands) * d[3];
+  if (units >= (1ll << 31)) return fail(LFBP_ERR_UNSUPPORTED, "too many work units (%lld)", (long long)units);
+  p.n_units = units;
+  int per_sm = 0;
+  if (dp.real) {
+    cudaError_t e = (E == 4) ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hp::hprime_kernel<4>,
+                                                                           threads, p.smem_bytes)
+                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hp::hprime_kernel<8>,
+                                                                           threads, p.smem_bytes);
+    if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "occupancy query: %s", cudaGetErrorString(e));
+  } else {
+    per_sm = std::min<int>(dp.max_threads_sm / threads, int((233472) / (p.smem_bytes + 1024)));
+  }
+  const int cap = env_int("LFBP_CTAS_PER_SM", 0);
+  if (cap > 0) per_sm = std::min(per_sm, cap);
+  if (per_sm < 1) return fail(LFBP_ERR_UNSUPPORTED, "kernel does not fit on an SM");
+  p.ctas_per_sm = per_sm;
+  p.grid = static_cast<int32_t>(std::min<int64_t>(units, int64_t(per_sm) * dp.sm_count));
+  p.nx_div = hp_fastdiv_make(static_cast<uint32_t>(d[2]));
+  p.ny_div = hp_fastdiv_make(static_cast<uint32_t>(d[3]));
+  p.nb_div = hp_fastdiv_make(static_cast<uint32_t>(p.n_bands));
+  p.nc_div = hp_fastdiv_make(static_cast<uint32_t>(p.n_chunks));
+  return LFBP_OK;
+}
+
+int launch(const HpPlan& p, const void* src, void* dst, cudaStream_t st) {
+  if (p.n_units == 0) return LFBP_OK;
+  if (p.elem == 4)
+    hp::hprime_kernel<4><<<p.grid, p.threads, p.smem_bytes, st>>>(p, static_cast<const uint8_t*>(src),
+                                                                   static_cast<uint8_t*>(dst));
+  else
+    hp::hprime_kernel<8><<<p.grid, p.threads, p.smem_bytes, st>>>(p, static_cast<const uint8_t*>(src),
+                                                                   static_cast<uint8_t*>(dst));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  HP_CUDA(cudaGetLastError());
+  return LFBP_OK;
+}
+
+int check_common(const int64_t dims[5], int dtype, int inverse) {
+  if (!dims) return fail(LFBP_ERR_ARGUMENT, "dims is NULL");
+  if (!hp_dims_valid(dims[0], dims[1], dims[2], dims[3], dims[4]))
+    return fail(LFBP_ERR_INVALID_DIMS, "invalid dims (%lld, %lld, %lld, %lld, %lld)", (long long)dims[0],
+                (long long)dims[1], (long long)dims[2], (long long)dims[3], (long long)dims[4]);
+  if (!elem_size(dtype)) return fail(LFBP_ERR_ARGUMENT, "dtype code %d is not 1 (f32) or 2 (f64)", dtype);
+  if (inverse && ((dims[0] % 2) == 0 || (dims[1] % 2) == 0))
+    return fail(LFBP_ERR_EVEN_PIXEL_DIMS,
+                "inverse undefined for even pixel dims (n_s, n_t)=(%lld, %lld): the forward mapping drops "
+                "elements",
+                (long long)dims[0], (long long)dims[1]);
+  return LFBP_OK;
+}
+
+int64_t plane_elems(const int64_t d[5]) { return d[0] * d[1] * d[2] * d[3]; }
+
+// ---- host pipeline workspace (one per device, reused across calls) ----
+constexpr int kPipe = 3;
+
+struct Workspace {
+  std::mutex mu;
+  int dev = -1;
+  size_t cap = 0;
+  void* in[kPipe] = {};
+  void* out[kPipe] = {};
+  cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
+  cudaEvent_t h2d_done[kPipe] = {}, cmp_done[kPipe] = {}, d2h_done[kPipe] = {};
+  bool init = false;
+};
+
+std::mutex g_ws_mu;
+std::map<int, std::unique_ptr<Workspace>> g_ws;
+
+Workspace& workspace(int dev) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto& w = g_ws[dev];
+  if (!w) {
+    w.reset(new Workspace());
+    w->dev = dev;
+  }
+  return *w;
+}
+
+int ws_reserve(Workspace& w, size_t bytes) {
+  if (!w.init) {
+    HP_CUDA(cudaStreamCreateWithFlags(&w.s_h2d, cudaStreamNonBlocking));
+    HP_CUDA(cudaStreamCreateWithFlags(&w.s_cmp, cudaStreamNonBlocking));
+    HP_CUDA(cudaStreamCreateWithFlags(&w.s_d2h, cudaStreamNonBlocking));
+    for (int k = 0; k < kPipe; ++k) {
+      HP_CUDA(cudaEventCreateWithFlags(&w.h2d_done[k], cudaEventDisableTiming));
+      HP_CUDA(cudaEventCreateWithFlags(&w.cmp_done[k], cudaEventDisableTiming));
+      HP_CUDA(cudaEventCreateWithFlags(&w.d2h_done[k], cudaEventDisableTiming));
+    }
+    w.init = true;
+  }
+  if (bytes <= w.cap) return LFBP_OK;
+  for (int k = 0; k < kPipe; ++k) {
+    if (w.in[k]) cudaFree(w.in[k]);
+    if (w.out[k]) cudaFree(w.out[k]);
+    w.in[k] = w.out[k] = nullptr;
+  }
+  w.cap = 0;
+  for (int k = 0; k < kPipe; ++k) {
+    HP_CUDA(cudaMalloc(&w.in[k], bytes));
+    HP_CUDA(cudaMalloc(&w.out[k], bytes));
+  }
+  w.cap = bytes;
+  return LFBP_OK;
+}
+
+struct HostPin {
+  void* ptr = nullptr;
+  bool registered = false;
+  ~HostPin() {
+    if (registered) cudaHostUnregister(ptr);
+  }
+};
+
+int maybe_pin(HostPin& pin, const void* p, size_t bytes, int flags) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    a.type = cudaMemoryTypeUnregistered;
+  }
+  if (a.type != cudaMemoryTypeUnregistered || !(flags & LFBP_HOST_REGISTER)) return LFBP_OK;
+  cudaError_t e = cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return LFBP_OK;
+  }
+  if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+  pin.ptr = const_cast<void*>(p);
+  pin.registered = true;
+  return LFBP_OK;
+}
+
+// planes [z0, z1) of host src -> host dst through device `dev`
+int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, int dev, int64_t z0, int64_t z1,
+              int flags) {
+  HP_CUDA(cudaSetDevice(dev));
+  const int64_t pb = plane_elems(dims) * E;
+  const int64_t nz = z1 - z0;
+  if (nz <= 0) return LFBP_OK;
+  const int64_t target = int64_t(env_int("LFBP_CHUNK_MB", 64)) << 20;
+  const int64_t cp = std::max<int64_t>(1, std::min<int64_t>(nz, target / std::max<int64_t>(pb, 1)));
+  const int64_t n_chunks = (nz + cp - 1) / cp;
+  HostPin pin_in, pin_out;
+  int rc = maybe_pin(pin_in, src + z0 * pb, size_t(nz * pb), flags);
+  if (rc) return rc;
+  rc = maybe_pin(pin_out, dst + z0 * pb, size_t(nz * pb), flags);
+  if (rc) return rc;
+  Workspace& w = workspace(dev);
+  std::lock_guard<std::mutex> lk(w.mu);
+  rc = ws_reserve(w, size_t(cp * pb));
+  if (rc) return rc;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int k = int(c % kPipe);
+    const int64_t a = z0 + c * cp, planes = std::min<int64_t>(cp, z1 - a);
+    const size_t bytes = size_t(planes * pb);
+    if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_h2d, w.cmp_done[k], 0));  // in[k] consumed
+    HP_CUDA(cudaMemcpyAsync(w.in[k], src + a * pb, bytes, cudaMemcpyHostToDevice, w.s_h2d));
+    HP_CUDA(cudaEventRecord(w.h2d_done[k], w.s_h2d));
+    HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.h2d_done[k], 0));
+    if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.d2h_done[k], 0));  // out[k] drained
+    int64_t cd[5] = {dims[0], dims[1], dims[2], dims[3], planes};
+    HpPlan p;
+    rc = make_plan(p, cd, E, 0, planes, int64_t(bytes), dev);
+    if (rc) return rc;
+    rc = launch(p, w.in[k], w.out[k], w.s_cmp);
+    if (rc) return rc;
+    HP_CUDA(cudaEventRecord(w.cmp_done[k], w.s_cmp));
+    HP_CUDA(cudaStreamWaitEvent(w.s_d2h, w.cmp_done[k], 0));
+    HP_CUDA(cudaMemcpyAsync(dst + a * pb, w.out[k], bytes, cudaMemcpyDeviceToHost, w.s_d2h));
+    HP_CUDA(cudaEventRecord(w.d2h_done[k], w.s_d2h));
+  }
+  HP_CUDA(cudaStreamSynchronize(w.s_d2h));
+  HP_CUDA(cudaStreamSynchronize(w.s_cmp));
+  HP_CUDA(cudaStreamSynchronize(w.s_h2d));
+  return LFBP_OK;
+}
+
+// ---- K2: device bitwise comparator ----
+__global__ void compare_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int64_t n,
+                               unsigned long long* n_diff, unsigned long long* first) {
+  const int64_t n16 = n / 16;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  unsigned long long cnt = 0, fst = ~0ull;
+  const uint4* a4 = reinterpret_cast<const uint4*>(a);
+  const uint4* b4 = reinterpret_cast<const uint4*>(b);
+  for (int64_t k = tid; k < n16; k += stride) {
+    const uint4 x = a4[k], y = b4[k];
+    const uint32_t w[4] = {x.x ^ y.x, x.y ^ y.y, x.z ^ y.z, x.w ^ y.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (w[q]) {
+        for (int byte = 0; byte < 4; ++byte)
+          if ((w[q] >> (8 * byte)) & 0xff) {
+            ++cnt;
+            fst = min(fst, (unsigned long long)(k * 16 + q * 4 + byte));
+          }
+      }
+    }
+  }
+  for (int64_t k = n16 * 16 + tid; k < n; k += stride)
+    if (a[k] != b[k]) {
+      ++cnt;
+      fst = min(fst, (unsigned long long)k);
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    fst = min(fst, __shfl_xor_sync(0xffffffffu, fst, o));
+  }
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd(n_diff, cnt);
+    atomicMin(first, fst);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int lfbp_check_dims(const int64_t dims[5]) {
+  if (!dims) return fail(LFBP_ERR_ARGUMENT, "dims is NULL");
+  if (!hp_dims_valid(dims[0], dims[1], dims[2], dims[3], dims[4]))
+    return fail(LFBP_ERR_INVALID_DIMS, "invalid dims");
+  return LFBP_OK;
+}
+
+int64_t lfbp_dropped_source_count(const int64_t d[5]) {
+  if (!d || !hp_dims_valid(d[0], d[1], d[2], d[3], d[4])) return -1;
+  const int64_t v_s = d[0] - (1 - d[0] % 2), v_t = d[1] - (1 - d[1] % 2);
+  return (d[0] * d[1] - v_s * v_t) * d[2] * d[3] * d[4];
+}
+
+int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse,
+                       int64_t z_begin, int64_t z_end, void* stream) {
+  int rc = check_common(dims, dtype, inverse);
+  if (rc) return rc;
+  if (!src || !dst) return fail(LFBP_ERR_ARGUMENT, "null device pointer");
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return fail(LFBP_ERR_ARGUMENT, "device arrays must be 16-byte aligned");
+  if (z_begin < 0 || z_end > dims[4] || z_begin > z_end)
+    return fail(LFBP_ERR_ARGUMENT, "plane range [%lld, %lld) outside [0, %lld)", (long long)z_begin,
+                (long long)z_end, (long long)dims[4]);
+  const int E = elem_size(dtype);
+  const int64_t total = plane_elems(dims) * dims[4] * E;
+  const uint8_t* s8 = static_cast<const uint8_t*>(src);
+  uint8_t* d8 = static_cast<uint8_t*>(dst);
+  if (s8 < d8 + total && d8 < s8 + total) return fail(LFBP_ERR_ARGUMENT, "src and dst overlap");
+  int dev = 0;
+  HP_CUDA(cudaGetDevice(&dev));
+  HpPlan p;
+  rc = make_plan(p, dims, E, z_begin, z_end - z_begin, total, dev);
+  if (rc) return rc;
+  return launch(p, src, dst, static_cast<cudaStream_t>(stream));
+}
+
+int lfbp_hprime_host(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse, int device,
+                     int flags) {
+  int rc = check_common(dims, dtype, inverse);
+  if (rc) return rc;
+  if (!src || !dst) return fail(LFBP_ERR_ARGUMENT, "null host pointer");
+  const int E = elem_size(dtype);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  rc = host_slab(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), dims, E, device, 0, dims[4],
+                 flags);
+  cudaSetDevice(cur);
+  return rc;
+}
+
+int lfbp_shard_planes(int64_t n_z, int n_shards, int shard, int64_t* z_begin, int64_t* z_end) {
+  if (n_z < 0 || n_shards < 1 || shard < 0 || shard >= n_shards || !z_begin || !z_end)
+    return fail(LFBP_ERR_ARGUMENT, "bad shard request");
+  *z_begin = (n_z * shard) / n_shards;
+  *z_end = (n_z * (shard + 1)) / n_shards;
+  return LFBP_OK;
+}
+
+int lfbp_hprime_multi(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse, int n_devices,
+                      const int* devices, int flags) {
+  int rc = check_common(dims, dtype, inverse);
+  if (rc) return rc;
+  if (!src || !dst || n_devices < 1 || !devices) return fail(LFBP_ERR_ARGUMENT, "bad multi-GPU arguments");
+  const int E = elem_size(dtype);
+  // pin once for all devices (portable registration); slabs then skip it
+  const size_t total = size_t(plane_elems(dims) * dims[4] * E);
+  HostPin pin_in, pin_out;
+  rc = maybe_pin(pin_in, src, total, flags);
+  if (rc) return rc;
+  rc = maybe_pin(pin_out, dst, total, flags);
+  if (rc) return rc;
+  const int slab_flags = flags & ~LFBP_HOST_REGISTER;
+  std::vector<int> codes(n_devices, LFBP_OK);
+  std::vector<std::string> msgs(n_devices);
+  std::vector<std::thread> th;
+  for (int g = 0; g < n_devices; ++g) {
+    int64_t z0, z1;
+    lfbp_shard_planes(dims[4], n_devices, g, &z0, &z1);
+    th.emplace_back([&, g, z0, z1] {
+      codes[g] = host_slab(static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), dims, E, devices[g],
+                           z0, z1, slab_flags);
+      if (codes[g]) msgs[g] = g_err;
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int g = 0; g < n_devices; ++g)
+    if (codes[g]) return fail(codes[g], "device %d: %s", devices[g], msgs[g].c_str());
+  return LFBP_OK;
+}
+
+int lfbp_compare_device(const void* a, const void* b, int64_t nbytes, int64_t* n_diff, int64_t* first_diff,
+                        void* stream) {
+  if (!a || !b || nbytes < 0 || !n_diff || !first_diff) return fail(LFBP_ERR_ARGUMENT, "bad compare arguments");
+  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)
+    return fail(LFBP_ERR_ARGUMENT, "compare buffers must be 16-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* scratch = nullptr;
+  HP_CUDA(cudaMalloc(&scratch, 2 * sizeof(unsigned long long)));
+  unsigned long long init[2] = {0ull, ~0ull};
+  cudaError_t e = cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const DevProps dp = device_props(dev);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(dp.sm_count) * 8, (nbytes / 16 + 255) / 256));
+    compare_kernel<<<int(blocks), 256, 0, st>>>(static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b),
+                                                nbytes, scratch, scratch + 1);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+  }
+  unsigned long long res[2] = {0ull, ~0ull};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(res, scratch, sizeof(res), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(scratch);
+  if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "compare: %s", cudaGetErrorString(e));
+  *n_diff = int64_t(res[0]);
+  *first_diff = res[0] ? int64_t(res[1]) : -1;
+  return LFBP_OK;
+}
+
+int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len) {
+  int rc = check_common(dims, dtype, 0);
+  if (rc) return rc;
+  if (!buf || buf_len < 1) return fail(LFBP_ERR_ARGUMENT, "null buffer");
+  int dev = 0;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    dev = -1;
+  } else {
+    cudaGetDevice(&dev);
+  }
+  const int E = elem_size(dtype);
+  HpPlan p;
+  rc = make_plan(p, dims, E, 0, dims[4], plane_elems(dims) * dims[4] * E, dev);
+  if (rc) return rc;
+  const DevProps dp = device_props(dev);
+  int w = snprintf(buf, size_t(buf_len),
+                   "{\"elem\": %d, \"J\": %d, \"n_bands\": %d, \"C\": %d, \"n_chunks\": %d, \"row_pitch\": %d, "
+                   "\"stage_bytes\": %d, \"stages\": %d, \"threads\": %d, \"smem_bytes\": %d, \"ctas_per_sm\": %d, "
+                   "\"grid\": %d, \"n_units\": %lld, \"sm_count\": %d, \"device_props\": \"%s\"}",
+                   p.elem, p.J, p.n_bands, p.C, p.n_chunks, p.row_pitch, p.stage_bytes, p.stages, p.threads,
+                   p.smem_bytes, p.ctas_per_sm, p.grid, (long long)p.n_units, dp.sm_count,
+                   dp.real ? "queried" : "b200-defaults");
+  if (w < 0 || w >= buf_len) return fail(LFBP_ERR_ARGUMENT, "buffer too small");
+  return LFBP_OK;
+}
+
+int64_t lfbp_launch_count(void) { return g_launches.load(); }
+
+const char* lfbp_last_error(void) { return g_err.c_str(); }
+
+const char* lfbp_version(void) { return "lfbp-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+"""Verification harness for the device path (reference: bench.py:88's
+bitwise ``np.array_equal`` and ``lfbp verify``, cli.py:129-150).
+
+* ``compare_device(a, b)`` -- K2 kernel: number of differing bytes and the
+  first differing byte offset of two device buffers.
+* ``first_mismatch_index(shape, byte_offset, itemsize)`` -- 0-based
+  (s, t, x, y, z) of a byte offset in the F-ordered array, the way
+  ``lfbp verify`` reports the first differing element (cli.py:145-150).
+* ``plane_digests(t)`` -- per-plane SHA-256 of a device array (planes are
+  copied to the host one at a time), comparable with the reference-produced
+  golden digests under ``tests/golden/``.
+* ``involution_check(h)`` -- applies the kernel twice on the device and
+  compares with the input (odd n_s, n_t: the map is an involution,
+  reference test_transform.py:157-162).
+* ``negative_control(h, hp)`` -- flips one bit of a copy of ``hp`` and
+  asserts the comparator catches it.
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+
+from . import _native
+from .errors import VerificationFailure
+
+
+def compare_device(a, b, stream=None) -> tuple[int, int]:
+    import torch
+    if a.numel() * a.element_size() != b.numel() * b.element_size():
+        raise ValueError("buffers differ in size")
+    nbytes = a.numel() * a.element_size()
+    n_diff = ctypes.c_int64(0)
+    first = ctypes.c_int64(-1)
+    if stream is None:
+        stream = torch.cuda.current_stream(a.device)
+    with torch.cuda.device(a.device):
+        rc = _native.lib().lfbp_compare_device(ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(b.data_ptr()),
+                                               nbytes, ctypes.byref(n_diff), ctypes.byref(first),
+                                               ctypes.c_void_p(stream.cuda_stream))
+    _native.check(rc)
+    return int(n_diff.value), int(first.value)
+
+
+def first_mismatch_index(shape, byte_offset: int, itemsize: int) -> tuple[int, ...]:
+    e = byte_offset // itemsize
+    idx = []
+    for n in shape:
+        idx.append(e % n)
+        e //= n
+    return tuple(idx)
+
+
+def plane_digests(t, shape) -> list[str]:
+    """SHA-256 of each z-plane's bytes of a device tensor in F layout."""
+    import torch
+    n_s, n_t, n_x, n_y, n_z = shape
+    flat = t.reshape(-1) if t.is_contiguous() else t.permute(4, 3, 2, 1, 0).reshape(-1)
+    per = n_s * n_t * n_x * n_y
+    host = torch.empty(per, dtype=t.dtype, pin_memory=True)
+    out = []
+    for z in range(n_z):
+        host.copy_(flat[z * per:(z + 1) * per])
+        out.append(hashlib.sha256(host.numpy().tobytes()).hexdigest())
+    return out
+
+
+def involution_check(h, scratch=None) -> tuple[int, int]:
+    """(n_diff, first) of rearrange(rearrange(h)) vs h, all on the device."""
+    from .transform import hprime_device
+    hp = hprime_device(h)
+    back = hprime_device(hp, out=scratch)
+    return compare_device(back, h)
+
+
+def negative_control(hp) -> None:
+    """A one-bit flip in a copy of ``hp`` must be detected by the comparator."""
+    import torch
+    bad = hp.clone()
+    raw = bad.view(torch.uint8) if bad.is_contiguous() else bad.permute(4, 3, 2, 1, 0).view(torch.uint8)
+    flat = raw.reshape(-1)
+    pos = flat.numel() // 2 + 3
+    flat[pos] ^= 0x10
+    n_diff, first = compare_device(hp, bad)
+    if n_diff != 1 or first != pos:
+        raise VerificationFailure(f"negative control not caught: n_diff={n_diff} first={first} pos={pos}")

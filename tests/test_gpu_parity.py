@@ -1,0 +1,227 @@
+"""Parity of the CUDA path with the reference (GPU; run with -m gpu).
+
+Every comparison is byte-for-byte: against the reference-produced golden
+arrays (tests/golden/small_cases.npz), against the reference's per-plane
+SHA-256 digests for the BASELINE configs (tests/golden/digests_C*.json), and
+against the CPU oracle (oracle/hprime_oracle.py) on seeded inputs.
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import load_digests
+from oracle.hprime_oracle import hprime_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def to_device(H):
+    """F-ordered numpy array -> CUDA tensor (n_s..n_z) with F strides."""
+    torch = _torch()
+    flat = torch.from_numpy(np.ascontiguousarray(H.reshape(-1, order="F")))
+    return flat.cuda().view(H.shape[::-1]).permute(4, 3, 2, 1, 0)
+
+
+def to_host(t):
+    """CUDA tensor in F layout -> its F-order element stream (1-D numpy)."""
+    return t.permute(4, 3, 2, 1, 0).contiguous().cpu().numpy().reshape(-1)
+
+
+def fbytes(H):
+    return np.asarray(H).tobytes(order="F")
+
+
+def test_device_api_matches_every_small_golden_case(golden_small):
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device
+    cases, arrays = golden_small
+    for c in cases:
+        H = arrays[c["name"] + "__H"]
+        out = hprime_device(to_device(H))
+        torch.cuda.synchronize()
+        assert to_host(out).tobytes() == fbytes(arrays[c["name"] + "__Hp"]), c["name"]
+        if c["inverse"]:
+            inv = hprime_device(to_device(H), inverse=True)
+            torch.cuda.synchronize()
+            assert to_host(inv).tobytes() == fbytes(arrays[c["name"] + "__Hinv"]), c["name"]
+
+
+def test_dropin_host_path_matches_every_small_golden_case(golden_small, caplog):
+    _torch()
+    import logging
+
+    from paper_2003_09133_b200 import (BackprojArray, Dims5, PsfArray, compute_backprojection,
+                                       compute_psf_from_backprojection)
+    cases, arrays = golden_small
+    for c in cases:
+        H = arrays[c["name"] + "__H"]
+        dims = Dims5(*c["shape"])
+        with caplog.at_level(logging.WARNING):
+            caplog.clear()
+            bp = compute_backprojection(PsfArray._wrap(dims, H))
+        assert isinstance(bp, BackprojArray)
+        assert bp.data.flags.f_contiguous and not bp.data.flags.writeable
+        assert bp.dtype == H.dtype
+        assert fbytes(bp.data) == fbytes(arrays[c["name"] + "__Hp"]), c["name"]
+        assert ("dropped" in caplog.text) == (c["dropped"] > 0)
+        if c["inverse"]:
+            psf = compute_psf_from_backprojection(BackprojArray._wrap(dims, H))
+            assert isinstance(psf, PsfArray)
+            assert fbytes(psf.data) == fbytes(arrays[c["name"] + "__Hinv"]), c["name"]
+
+
+def test_inverse_refused_for_even_dims():
+    _torch()
+    from paper_2003_09133_b200 import (BackprojArray, Dims5, EvenPixelDims, compute_psf_from_backprojection,
+                                       hprime_device)
+    H = np.ones((4, 5, 3, 3, 1), order="F")
+    with pytest.raises(EvenPixelDims):
+        compute_psf_from_backprojection(BackprojArray._wrap(Dims5(4, 5, 3, 3, 1), H))
+    with pytest.raises(EvenPixelDims):
+        hprime_device(to_device(H), inverse=True)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4", "C3"])
+def test_baseline_config_matches_reference_digests(cfg):
+    """Full-size BASELINE configs: every plane of the device H' has the SHA-256
+    of the reference's H' (computed by lfbp itself, tests/golden/)."""
+    torch = _torch()
+    from paper_2003_09133_b200 import f_order_empty, hprime_device
+    from paper_2003_09133_b200.configs import WORKLOADS
+    from paper_2003_09133_b200.synth import baseline_psf
+    from paper_2003_09133_b200.verify import plane_digests
+    d = load_digests(cfg)
+    if d is None:
+        pytest.skip(f"digests_{cfg}.json not generated")
+    w = WORKLOADS[cfg]
+    tdt = torch.float32 if w.itemsize == 4 else torch.float64
+    src = f_order_empty(w.shape, tdt)
+    # generate plane slabs on the host and upload (the generator is pinned by digests)
+    step = max(1, (512 << 20) // (w.plane_elems * w.itemsize))
+    flat = src.permute(4, 3, 2, 1, 0).reshape(-1)
+    for z0 in range(0, w.shape[4], step):
+        z1 = min(w.shape[4], z0 + step)
+        slab = baseline_psf(w, z0, z1)
+        flat[z0 * w.plane_elems:z1 * w.plane_elems].copy_(torch.from_numpy(slab.reshape(-1, order="F")))
+    in_dig = plane_digests(src, w.shape)
+    assert in_dig == d["input_plane_sha256"]
+    out = hprime_device(src)
+    torch.cuda.synchronize()
+    got = plane_digests(out, w.shape)
+    bad = [z for z in range(w.shape[4]) if got[z] != d["hprime_plane_sha256"][z]]
+    assert not bad, f"{cfg}: planes {bad[:8]} differ from the reference"
+
+
+@pytest.mark.parametrize("shape,dtype", [
+    ((55, 55, 11, 11, 3), np.float32), ((195, 195, 15, 15, 2), np.float32), ((273, 273, 13, 13, 2), np.float64),
+    ((181, 181, 95, 55, 1), np.float32), ((8, 12, 7, 3, 3), np.float32), ((10, 5, 5, 5, 2), np.float64),
+    ((1, 1, 1, 1, 3), np.float32), ((3, 3, 1, 1, 5), np.float64), ((89, 91, 11, 13, 2), np.float32),
+    ((31, 17, 31, 17, 2), np.float32), ((400, 6, 399, 5, 1), np.float64),
+])
+def test_random_shapes_match_oracle(shape, dtype):
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    H = random_psf_like_reference(shape, density=0.5, seed=sum(shape), dtype=dtype)
+    want = hprime_oracle(H)
+    out = hprime_device(to_device(H))
+    torch.cuda.synchronize()
+    assert to_host(out).tobytes() == fbytes(want)
+    if shape[0] % 2 and shape[1] % 2:
+        back = hprime_device(out, inverse=True)
+        torch.cuda.synchronize()
+        assert to_host(back).tobytes() == fbytes(H)
+
+
+@pytest.mark.parametrize("env", [
+    {"LFBP_STAGE_MAX_KB": "4"},            # forces the i-chunked path
+    {"LFBP_STAGES": "1"}, {"LFBP_STAGES": "2", "LFBP_THREADS": "64"},
+    {"LFBP_STAGE_KB": "1"}, {"LFBP_STAGE_KB": "200", "LFBP_STAGE_MAX_KB": "200"},
+    {"LFBP_CTAS_PER_SM": "1", "LFBP_THREADS": "512"}, {"LFBP_BAND": "3"},
+])
+@pytest.mark.parametrize("shape,dtype", [((55, 55, 11, 11, 2), np.float32), ((27, 20, 13, 5, 2), np.float64),
+                                         ((66, 41, 21, 9, 1), np.float32)])
+def test_plan_variants_are_bit_exact(monkeypatch, env, shape, dtype):
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device, plan
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    p = plan(shape, dtype)
+    if env.get("LFBP_STAGE_MAX_KB") == "4":
+        assert p["n_chunks"] > 1
+    H = random_psf_like_reference(shape, density=0.9, seed=7, dtype=dtype)
+    out = hprime_device(to_device(H))
+    torch.cuda.synchronize()
+    assert to_host(out).tobytes() == fbytes(hprime_oracle(H))
+
+
+def test_z_range_writes_only_its_planes():
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    shape = (21, 19, 7, 5, 6)
+    H = random_psf_like_reference(shape, density=1.0, seed=3, dtype=np.float32)
+    src = to_device(H)
+    out = torch.full_like(src, -7.0)
+    hprime_device(src, out=out, z_range=(2, 5))
+    torch.cuda.synchronize()
+    got = to_host(out).reshape(shape, order="F")
+    want = hprime_oracle(H)
+    assert fbytes(got[..., 2:5]) == fbytes(want[..., 2:5])
+    assert (got[..., :2] == -7.0).all() and (got[..., 5:] == -7.0).all()
+
+
+def test_unaligned_total_size_tail_loads():
+    """Arrays whose byte size is not a multiple of 16 (tail words loaded
+    without bulk copies), in an exact-size allocation."""
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    for shape in [(5, 3, 3, 3, 1), (7, 5, 5, 3, 3), (3, 3, 3, 3, 1)]:
+        H = random_psf_like_reference(shape, density=1.0, seed=5, dtype=np.float32)
+        assert H.nbytes % 16 != 0
+        out = hprime_device(to_device(H))
+        torch.cuda.synchronize()
+        assert to_host(out).tobytes() == fbytes(hprime_oracle(H))
+
+
+def test_verification_harness_involution_and_negative_control():
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device
+    from paper_2003_09133_b200.configs import WORKLOADS
+    from paper_2003_09133_b200.synth import baseline_psf
+    from paper_2003_09133_b200.verify import compare_device, first_mismatch_index, involution_check, negative_control
+    w = WORKLOADS["C1"]
+    src = to_device(baseline_psf(w))
+    n, first = involution_check(src)
+    assert (n, first) == (0, -1)
+    hp = hprime_device(src)
+    negative_control(hp)
+    n, first = compare_device(hp, src)
+    assert n > 0 and first >= 0
+    assert len(first_mismatch_index(w.shape, first, 4)) == 5
+
+
+def test_multi_device_host_launcher_single_gpu():
+    torch = _torch()
+    from paper_2003_09133_b200.shard import rearrange_multi_host
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    shape = (33, 29, 11, 9, 7)
+    H = random_psf_like_reference(shape, density=1.0, seed=9, dtype=np.float32)
+    out = np.empty_like(H, order="F")
+    rearrange_multi_host(H, out, [0])
+    assert fbytes(out) == fbytes(hprime_oracle(H))
+    # the same device listed twice = two concurrent slabs on one GPU
+    out2 = np.empty_like(H, order="F")
+    rearrange_multi_host(H, out2, [0, 0])
+    assert fbytes(out2) == fbytes(out)

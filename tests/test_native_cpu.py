@@ -1,0 +1,118 @@
+"""The C-ABI library loads and exports every declared symbol; host-only
+entry points behave like the reference (no GPU needed, no compute calls)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2003_09133_b200 import Dims5, InvalidDims, _native, plan
+from paper_2003_09133_b200.configs import WORKLOADS
+from paper_2003_09133_b200.shard import imbalance, shard_planes
+
+
+def _declared():
+    names = set()
+    inc = os.path.join(ROOT, "include")
+    for fn in os.listdir(inc):
+        if fn.endswith(".h"):
+            text = open(os.path.join(inc, fn)).read()
+            names |= set(re.findall(r"^\s*(?:const\s+)?[\w\*]+\s+\*?(lfbp_\w+)\s*\(", text, re.M))
+    return names
+
+
+def test_library_exports_every_header_symbol():
+    lib = _native.lib()
+    declared = _declared()
+    assert len(declared) >= 11
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(_native.EXPORTS) == declared
+
+
+def test_version_and_no_error_initially():
+    assert b"sm_100a" in _native.lib().lfbp_version()
+
+
+@pytest.mark.parametrize("shape,ok", [
+    ((9, 7, 3, 7, 2), True), ((5, 5, 3, 3, 1), True), ((4, 5, 3, 3, 1), True), ((1, 1, 1, 1, 1), True),
+    ((9, 9, 4, 3, 1), False), ((9, 9, 3, 2, 1), False), ((2, 9, 3, 3, 1), False), ((9, 2, 3, 3, 1), False),
+    ((0, 9, 3, 3, 1), False), ((9, 9, 3, 3, 0), False), ((3, 3, 5, 3, 1), False),
+])
+def test_check_dims_matches_dims5(shape, ok):
+    rc = _native.lib().lfbp_check_dims(_native.dims_array(shape))
+    assert (rc == _native.OK) == ok
+    if ok:
+        Dims5(*shape)
+    else:
+        assert rc == _native.ERR_INVALID_DIMS
+        with pytest.raises(InvalidDims):
+            Dims5(*shape)
+
+
+def test_dropped_source_count():
+    f = _native.lib().lfbp_dropped_source_count
+    assert f(_native.dims_array((4, 5, 3, 3, 1))) == 45
+    assert f(_native.dims_array((9, 9, 3, 3, 3))) == 0
+    assert f(_native.dims_array((6, 6, 3, 5, 2))) == (36 - 25) * 15 * 2
+    assert f(_native.dims_array((4, 4, 4, 3, 1))) == -1
+
+
+def test_shard_planes_c_and_python_agree():
+    for n_z in (1, 9, 51, 64, 41, 101):
+        for g in (1, 2, 4, 8):
+            cover = []
+            for k in range(g):
+                a, b = ctypes.c_int64(), ctypes.c_int64()
+                assert _native.lib().lfbp_shard_planes(n_z, g, k, ctypes.byref(a), ctypes.byref(b)) == 0
+                assert (a.value, b.value) == shard_planes(n_z, g, k)
+                cover.extend(range(a.value, b.value))
+            assert cover == list(range(n_z))
+    assert imbalance(64, 8) == 1.0
+    assert abs(imbalance(51, 8) - 7 / (51 / 8)) < 1e-12
+
+
+@pytest.mark.parametrize("cfg", list(WORKLOADS))
+def test_plans_for_every_config_fit_b200(cfg):
+    w = WORKLOADS[cfg]
+    p = plan(w.shape, w.dtype)
+    assert p["smem_bytes"] <= 232448
+    assert p["stages"] >= 2 and p["grid"] >= 148
+    assert p["n_units"] < 2 ** 31
+    assert p["row_pitch"] % 16 == 0
+    # one staged unit holds J full rows per x (or an i-chunk)
+    n_s = w.shape[0]
+    assert p["row_pitch"] >= min(p["J"] * n_s, p["C"]) * w.itemsize + 16
+
+
+def test_plan_chunks_huge_slabs():
+    p = plan((4001, 9, 2001, 3, 1), np.float64)
+    assert p["n_chunks"] > 1 and p["J"] == 1
+
+
+def test_compute_entry_points_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    buf = np.zeros(64, dtype=np.float32)
+    ptr = buf.ctypes.data_as(ctypes.c_void_p)
+    rc = _native.lib().lfbp_hprime_device(ptr, ptr, _native.dims_array((3, 3, 1, 1, 1)), 1, 0, 0, 1, None)
+    assert rc != _native.OK
+    out = np.zeros(64, dtype=np.float32)
+    rc = _native.lib().lfbp_hprime_host(ptr, out.ctypes.data_as(ctypes.c_void_p),
+                                        _native.dims_array((3, 3, 1, 1, 1)), 1, 0, 0, 0)
+    assert rc == _native.ERR_CUDA
+    assert _native.last_error()
+
+
+def test_argument_errors():
+    lib = _native.lib()
+    d = _native.dims_array((5, 5, 3, 3, 1))
+    assert lib.lfbp_hprime_device(None, None, d, 1, 0, 0, 1, None) == _native.ERR_ARGUMENT
+    assert lib.lfbp_hprime_device(None, None, d, 3, 0, 0, 1, None) == _native.ERR_ARGUMENT
+    assert lib.lfbp_hprime_device(None, None, _native.dims_array((4, 5, 3, 3, 1)), 1, 1, 0, 1, None) \
+        == _native.ERR_EVEN_PIXEL_DIMS
+    assert lib.lfbp_hprime_host(None, None, _native.dims_array((5, 5, 2, 3, 1)), 1, 0, 0, 0) \
+        == _native.ERR_INVALID_DIMS
