@@ -69,6 +69,15 @@ __device__ __forceinline__ void st_v2_64(void* p, unsigned long long a, unsigned
   asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
+__device__ __forceinline__ void st_v4_na(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_v2_64_na(void* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.global.L1::no_allocate.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
 struct Unit {
   int64_t z, y;
   int32_t t0, jb;        // band start and rows
@@ -105,26 +114,52 @@ __device__ __forceinline__ Unit decode_unit(const HpPlan& p, uint32_t u) {
   return w;
 }
 
-// Producer: stage the n_x source runs of unit `u` into `stage`; arrival on `bar`.
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// Producer warp: stage the n_x source runs of unit `u` into `stage`, one
+// run per lane (x = lane, lane + 32, ...), completion on `bar`.
 template <int E>
 __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __restrict__ src, uint32_t u,
-                                           uint8_t* stage, uint32_t bar) {
+                                           uint8_t* stage, uint32_t bar, int lane, uint64_t policy) {
   using T = typename Word<E>::T;
   const Unit w = decode_unit(p, u);
   const int64_t run_bytes = w.run_elems * E;
   const int64_t xstride = p.n_s * p.n_t * E;
   const int64_t lim = p.total_bytes & ~int64_t(15);
+  const int64_t b0 = w.run_off0 * E;
   uint32_t tx = 0;
-  int64_t b = w.run_off0 * E;
   if (run_bytes > 0) {
-    for (int32_t x = 0; x < p.n_x; ++x, b += xstride) {
+    for (int32_t x = lane; x < p.n_x; x += 32) {
+      const int64_t b = b0 + x * xstride;
       const int64_t a_lo = b & ~int64_t(15);
       int64_t a_hi = (b + run_bytes + 15) & ~int64_t(15);
       if (a_hi > lim) a_hi = lim > a_lo ? lim : a_lo;
-      uint8_t* dst = stage + static_cast<int64_t>(x) * p.row_pitch;
+      // element k of run x lives at R0 + x*row_pitch + k*E (see hprime_plan.h);
+      // its 16-byte aligned superset starts (b & 15) bytes earlier
+      uint8_t* dst = stage + 16 + (b0 & 15) + static_cast<int64_t>(x) * p.row_pitch - (b & 15);
       if (a_hi > a_lo) {
         const uint32_t n = static_cast<uint32_t>(a_hi - a_lo);
-        bulk_g2s(smem_u32(dst), src + a_lo, n, bar);
+        if (p.flags & HP_FLAG_LOAD_EVICT_FIRST)
+          bulk_g2s_hint(smem_u32(dst), src + a_lo, n, bar, policy);
+        else
+          bulk_g2s(smem_u32(dst), src + a_lo, n, bar);
         tx += n;
       }
       // words past the last aligned 16 B of the allocation: plain loads
@@ -132,111 +167,152 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
         *reinterpret_cast<T*>(dst + (q - a_lo)) = *reinterpret_cast<const T*>(src + q);
     }
   }
-  mbar_arrive_expect_tx(bar, tx);  // tx-count may be transiently negative: legal
+  tx = __reduce_add_sync(0xffffffffu, tx);
+  __syncwarp();                                    // tail stores before the release
+  if (lane == 0) mbar_arrive_expect_tx(bar, tx);  // tx-count may be transiently negative: legal
 }
 
-// Consumers: all warps write the J * n_x output rows of unit `u` from `stage`.
+template <int E>
+__device__ __forceinline__ typename Word<E>::T lds(uint32_t addr) {
+  if constexpr (E == 4) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+  } else {
+    unsigned long long v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+  }
+}
+
+// Consumer warps (cw of nc) write the J * n_x output rows of unit `u`.
 template <int E>
 __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restrict__ dst, uint32_t u,
-                                             const uint8_t* stage) {
+                                             uint32_t stage_s, int cw, int nc, int lane) {
   using T = typename Word<E>::T;
   constexpr int VE = 16 / E;
   const Unit w = decode_unit(p, u);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int32_t n_x = static_cast<int32_t>(p.n_x);
-  const int32_t o0 = static_cast<int32_t>((w.run_off0 * E) & 15);
+  const int32_t rp = p.row_pitch;
+  const uint32_t base = stage_s + 16 + static_cast<uint32_t>((w.run_off0 * E) & 15);
+  const int32_t step = rp - E;                    // x -> x+1, s -> s-1
+  const int32_t wrap = step - n_x * rp;           // ... and x wraps to 0
+  const int32_t i_end = min(w.i_hi, p.v_s);       // loaded elements: [i_lo, i_end)
+  const int64_t xs = p.n_s * p.n_t;               // element stride of x'
   const int32_t rows = w.jb * n_x;
-  for (int32_t r = warp; r < rows; r += nwarps) {
+  for (int32_t r = cw; r < rows; r += nc) {
     const int32_t tl = static_cast<int32_t>(hp_div(p.nx_div, static_cast<uint32_t>(r)));
     const int32_t xp = r - tl * n_x;
     const int32_t t = w.t0 + tl;
-    int64_t j, yp;
     const bool zero_row = t >= p.v_t;  // dropped source row t = n_t - 1 (even n_t)
-    if (!zero_row) {
-      j = 2 * p.c_t - t;
-      yp = hp_mod(p.ny_div, static_cast<uint32_t>(w.y + t + p.ny_off));
-    } else {  // carries the all-zero output row j = n_t - 1 at y' = y
-      j = p.n_t - 1;
-      yp = w.y;
+    const int64_t j = zero_row ? p.n_t - 1 : 2 * p.c_t - t;
+    const int64_t yp = zero_row ? w.y : hp_mod(p.ny_div, static_cast<uint32_t>(w.y + t + p.ny_off));
+    const int64_t O = p.n_s * j + xs * (xp + p.n_x * (yp + p.n_y * w.z));
+    T* orow = reinterpret_cast<T*>(dst) + O;
+    if (zero_row) {
+      for (int32_t i = w.i_lo + lane; i < w.i_hi; i += 32) orow[i] = T(0);
+      continue;
     }
-    const int64_t O = p.n_s * (j + p.n_t * (xp + p.n_x * (yp + p.n_y * w.z)));
-    const int64_t e0 = O + w.i_lo, e1 = O + w.i_hi;
-    const int64_t g0 = e0 & ~int64_t(VE - 1);
-    const int32_t ng = static_cast<int32_t>((((e1 + VE - 1) & ~int64_t(VE - 1)) - g0) / VE);
-    const int32_t sbase = tl * static_cast<int32_t>(p.n_s) - w.s_lo;
-    for (int32_t g = lane; g < ng; g += 32) {
-      const int64_t ge = g0 + static_cast<int64_t>(g) * VE;
-      const int32_t i0 = static_cast<int32_t>(ge - O);
-      uint32_t x = hp_mod(p.nx_div, static_cast<uint32_t>(xp + i0 + p.nx_off + 4 * n_x));
+    if (i_end < w.i_hi && lane == 0) orow[p.n_s - 1] = T(0);  // even n_s: row i = n_s - 1 is zero
+    // element address of (x, i): base + x*rp + (tl*n_s - s_lo + 2c_s - i)*E
+    const int32_t k0 = tl * static_cast<int32_t>(p.n_s) - w.s_lo + 2 * p.c_s;
+    auto addr_of = [&](int32_t i, uint32_t& x) -> uint32_t {
+      x = hp_mod(p.nx_div, static_cast<uint32_t>(xp + i + p.nx_off));
+      return base + x * rp + (k0 - i) * E;
+    };
+    // head / body / tail split on the 16-byte grid of the output row
+    const int32_t mis = static_cast<int32_t>((O + w.i_lo) & (VE - 1));
+    const int32_t head = max(0, min(mis ? VE - mis : 0, i_end - w.i_lo));
+    const int32_t b0 = w.i_lo + head;
+    const int32_t nb = max(0, (i_end - b0) / VE);
+    const int32_t b1 = b0 + nb * VE;
+    // scalar head and tail (< VE elements each)
+    if (lane < head || (lane >= VE && lane - VE < i_end - b1)) {
+      const int32_t i = lane < head ? w.i_lo + lane : b1 + lane - VE;
+      uint32_t x;
+      orow[i] = lds<E>(addr_of(i, x));
+    }
+    for (int32_t g = lane; g < nb; g += 32) {
+      const int32_t i0 = b0 + g * VE;
+      uint32_t x;
+      uint32_t a = addr_of(i0, x);
       T v[VE];
-      bool ok[VE];
-      bool full = true;
 #pragma unroll
       for (int q = 0; q < VE; ++q) {
-        const int32_t i = i0 + q;
-        ok[q] = i >= w.i_lo && i < w.i_hi;
-        full = full && ok[q];
-        T val = 0;
-        if (ok[q] && !zero_row && i < p.v_s) {
-          const int32_t s = 2 * p.c_s - i;
-          const int32_t ox = (o0 + static_cast<int32_t>(x) * p.xs16) & 15;
-          const uint8_t* a = stage + static_cast<int32_t>(x) * p.row_pitch + ox + (sbase + s) * E;
-          val = *reinterpret_cast<const T*>(a);
-        }
-        v[q] = val;
-        x = (x + 1 == static_cast<uint32_t>(n_x)) ? 0u : x + 1;
+        v[q] = lds<E>(a);
+        const bool last = x == static_cast<uint32_t>(n_x - 1);
+        a += last ? wrap : step;
+        x = last ? 0u : x + 1;
       }
-      uint8_t* out = dst + ge * E;
-      if (full) {
+      if (p.flags & HP_FLAG_STORE_NA) {
         if constexpr (E == 4)
-          st_v4(out, v[0], v[1], v[2], v[3]);
+          st_v4_na(orow + i0, v[0], v[1], v[2], v[3]);
         else
-          st_v2_64(out, v[0], v[1]);
+          st_v2_64_na(orow + i0, v[0], v[1]);
       } else {
-#pragma unroll
-        for (int q = 0; q < VE; ++q)
-          if (ok[q]) reinterpret_cast<T*>(out)[q] = v[q];
+        if constexpr (E == 4)
+          st_v4(orow + i0, v[0], v[1], v[2], v[3]);
+        else
+          st_v2_64(orow + i0, v[0], v[1]);
       }
     }
   }
 }
 
+// Warp 0 (one elected lane) produces, warps 1.. consume; full/empty mbarrier
+// ring of `stages` buffers, so consumer warps never wait for each other.
 template <int E>
-__global__ void __launch_bounds__(512) hprime_kernel(const HpPlan p, const uint8_t* __restrict__ src,
+__global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8_t* __restrict__ src,
                                                      uint8_t* __restrict__ dst) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 8;
   uint8_t* stages = smem + 128;
-  const uint32_t first = blockIdx.x, step = gridDim.x;
+  const uint32_t first = blockIdx.x, stride = gridDim.x;
   if (first >= p.n_units) return;
   const uint32_t n_units = static_cast<uint32_t>(p.n_units);
-  const uint32_t mine = (n_units - first + step - 1) / step;
+  const uint32_t mine = (n_units - first + stride - 1) / stride;
   const int S = p.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nc = (blockDim.x >> 5) - 1;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), nc);
+    }
     fence_barrier_init();
-    const uint32_t pre = mine < static_cast<uint32_t>(S - 1) ? mine : static_cast<uint32_t>(S - 1);
-    for (uint32_t k = 0; k < pre; ++k)
-      issue_unit<E>(p, src, first + k * step, stages + static_cast<int64_t>(k) * p.stage_bytes,
-                    smem_u32(&bars[k]));
   }
   __syncthreads();
-  int st = 0;
-  uint32_t phase = 0;
-  for (uint32_t k = 0; k < mine; ++k) {
-    if (threadIdx.x == 0 && k + S - 1 < mine) {
-      int s2 = st + S - 1;
-      if (s2 >= S) s2 -= S;
-      fence_proxy_async_smem();  // order earlier generic reads of this buffer before the async writes
-      issue_unit<E>(p, src, first + (k + S - 1) * step, stages + static_cast<int64_t>(s2) * p.stage_bytes,
-                    smem_u32(&bars[s2]));
+  if (warp == 0) {
+    const uint64_t policy = policy_evict_first();
+    int st = 0;
+    uint32_t ph = 0;
+    for (uint32_t k = 0; k < mine; ++k) {
+      if (k >= static_cast<uint32_t>(S)) {
+        mbar_wait(smem_u32(&empty[st]), ph ^ 1u);
+        fence_proxy_async_smem();
+      }
+      issue_unit<E>(p, src, first + k * stride, stages + static_cast<int64_t>(st) * p.stage_bytes,
+                    smem_u32(&full[st]), lane, policy);
+      if (++st == S) {
+        st = 0;
+        ph ^= 1u;
+      }
     }
-    mbar_wait(smem_u32(&bars[st]), phase);
-    consume_unit<E>(p, dst, first + k * step, stages + static_cast<int64_t>(st) * p.stage_bytes);
-    __syncthreads();
+    return;
+  }
+  const uint32_t stage0 = smem_u32(stages);
+  int st = 0;
+  uint32_t ph = 0;
+  for (uint32_t k = 0; k < mine; ++k) {
+    mbar_wait(smem_u32(&full[st]), ph);
+    consume_unit<E>(p, dst, first + k * stride, stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - 1, nc,
+                    lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     if (++st == S) {
       st = 0;
-      phase ^= 1u;
+      ph ^= 1u;
     }
   }
 }

@@ -15,6 +15,13 @@
 // shared memory with 1-D bulk TMA.  Each staged run feeds J*n_x output rows
 // H'[i_lo:i_hi, j, x', y', z] with j = 2c_t - t and
 // y' = (y + t - c_t) mod n_y, written with 16-byte stores.
+//
+// Shared-memory layout of one stage: element k of the run of source phase x
+// sits at byte  R0 + x * row_pitch + k * elem,  R0 = 16 + (run byte offset
+// mod 16).  row_pitch is congruent to (n_s * n_t * elem) mod 16, so every
+// run's 16-byte-aligned superset lands on a 16-byte-aligned smem address (a
+// legal bulk-copy destination) while the element address stays LINEAR in x:
+// the consumer steps x -> x+1, s -> s-1 with one add.
 #pragma once
 #include <stdint.h>
 
@@ -56,6 +63,9 @@ HP_HD uint32_t hp_mod(const HpFastDiv& f, uint32_t n) {
   return n - hp_div(f, n) * f.d;
 }
 
+#define HP_FLAG_LOAD_EVICT_FIRST 1  // L2 evict_first hint on the bulk loads of H
+#define HP_FLAG_STORE_NA 2          // st.global.L1::no_allocate for H'
+
 struct HpPlan {
   // geometry of the (chunk) arrays the kernel sees
   int64_t n_s, n_t, n_x, n_y;
@@ -70,14 +80,15 @@ struct HpPlan {
   int32_t n_bands;            // ceil(n_t / J)
   int32_t C;                  // output i per unit (chunk); == n_s when unchunked
   int32_t n_chunks;           // ceil(n_s / C)
-  int32_t row_pitch;          // smem bytes per staged run (multiple of 16)
-  int32_t stage_bytes;        // n_x * row_pitch rounded to 128
+  int32_t row_pitch;          // smem bytes between staged runs (== xs16 mod 16)
+  int32_t stage_bytes;        // n_x * row_pitch + 32 rounded to 128
   int32_t stages;             // smem ring depth
-  int32_t threads;            // CTA size
+  int32_t threads;            // CTA size: 1 producer warp + consumer warps
   int32_t smem_bytes;         // dynamic smem per CTA
   int32_t grid;               // persistent CTAs
   int32_t ctas_per_sm;
   int32_t xs16;               // (n_s * n_t * elem) mod 16: run misalignment step per x
+  int32_t flags;              // HP_FLAG_*
   int64_t n_units;            // z_count * n_chunks * n_bands * n_y  (< 2^31)
   HpFastDiv nx_div;           // mod n_x on the element path
   HpFastDiv ny_div;           // unit decode / y' wrap

@@ -136,20 +136,24 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
     run_max = int64_t(p.C) * E;
   }
   p.n_bands = static_cast<int32_t>((d[1] + p.J - 1) / p.J);
+  // row pitch: >= run + 32 B, congruent to xs16 mod 16 (linear x addressing,
+  // see hprime_plan.h); the multiple-of-16 part is odd to spread banks
   int64_t pitch = round_up(run_max + 32, 16);
-  if (((pitch / 16) & 1) == 0) pitch += 16;  // odd multiple of 16 B spreads rows over banks
-  p.row_pitch = static_cast<int32_t>(pitch);
-  p.stage_bytes = static_cast<int32_t>(round_up(d[2] * pitch, 128));
-  int S = env_int("LFBP_STAGES", 3);
+  if (((pitch / 16) & 1) == 0) pitch += 16;
+  pitch += env_int("LFBP_PITCH_EXTRA16", 0) * 16;
+  p.row_pitch = static_cast<int32_t>(pitch + p.xs16);
+  p.stage_bytes = static_cast<int32_t>(round_up(d[2] * p.row_pitch + 32, 128));
+  int S = env_int("LFBP_STAGES", 4);
   S = std::max(1, std::min(S, 8));
   while (S > 1 && 128 + int64_t(S) * p.stage_bytes > dp.smem_optin) --S;
   if (128 + int64_t(S) * p.stage_bytes > dp.smem_optin)
     return fail(LFBP_ERR_UNSUPPORTED, "stage of %d bytes exceeds shared memory", p.stage_bytes);
   p.stages = S;
   p.smem_bytes = 128 + S * p.stage_bytes;
-  int threads = env_int("LFBP_THREADS", 0);
-  if (threads <= 0) threads = p.smem_bytes > dp.smem_optin / 2 ? 512 : 256;
-  threads = std::max(32, std::min(512, threads / 32 * 32));
+  int cwarps = env_int("LFBP_CONSUMER_WARPS", 0);
+  if (cwarps <= 0) cwarps = p.smem_bytes > dp.smem_optin / 2 ? 16 : 8;
+  cwarps = std::max(1, std::min(16, cwarps));
+  const int threads = 32 * (1 + cwarps);
   p.threads = threads;
 
   const int64_t units = z_count * p.n_chunks * int64_t(p.n_bands) * d[3];
@@ -170,6 +174,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   if (per_sm < 1) return fail(LFBP_ERR_UNSUPPORTED, "kernel does not fit on an SM");
   p.ctas_per_sm = per_sm;
   p.grid = static_cast<int32_t>(std::min<int64_t>(units, int64_t(per_sm) * dp.sm_count));
+  p.flags = env_int("LFBP_KFLAGS", 0);
   p.nx_div = hp_fastdiv_make(static_cast<uint32_t>(d[2]));
   p.ny_div = hp_fastdiv_make(static_cast<uint32_t>(d[3]));
   p.nb_div = hp_fastdiv_make(static_cast<uint32_t>(p.n_bands));

@@ -57,3 +57,28 @@ def rank_slab(shape, world_size: int, rank: int) -> tuple[tuple[int, ...], int, 
     """Shape of this rank's slab and its global plane range."""
     z0, z1 = shard_planes(shape[4], world_size, rank)
     return (shape[0], shape[1], shape[2], shape[3], z1 - z0), z0, z1
+
+
+def open_shared_host(path: str, shape, dtype, create: bool = False) -> np.ndarray:
+    """F-ordered host array backed by a shared file (e.g. under /dev/shm):
+    every rank maps the same H' and writes its own slab at byte offset
+    z0 * plane_bytes -- the final gather of the z-shards needs no network
+    collective."""
+    mode = "w+" if create else "r+"
+    return np.memmap(path, dtype=dtype, mode=mode, shape=tuple(shape), order="F")
+
+
+def write_slab(shared: np.ndarray, z0: int, slab: np.ndarray) -> None:
+    """Copy this rank's planes into the shared host array."""
+    z1 = z0 + slab.shape[4]
+    shared[..., z0:z1] = slab
+
+
+def device_slab_to_shared(shared: np.ndarray, z0: int, t) -> None:
+    """D2H of a device slab (F layout CUDA tensor) straight into the shared
+    host array at its plane offset."""
+    import torch
+    n = int(np.prod(t.shape))
+    flat_host = torch.from_numpy(shared.reshape(-1, order="F")[z0 * (n // t.shape[4]):][:n].view(np.uint8))
+    flat_dev = t.permute(4, 3, 2, 1, 0).reshape(-1).view(torch.uint8)
+    flat_host.copy_(flat_dev)

@@ -27,7 +27,7 @@ def _torch():
 def to_device(H):
     """F-ordered numpy array -> CUDA tensor (n_s..n_z) with F strides."""
     torch = _torch()
-    flat = torch.from_numpy(np.ascontiguousarray(H.reshape(-1, order="F")))
+    flat = torch.from_numpy(np.array(H.reshape(-1, order="F")))
     return flat.cuda().view(H.shape[::-1]).permute(4, 3, 2, 1, 0)
 
 
@@ -143,10 +143,10 @@ def test_random_shapes_match_oracle(shape, dtype):
 
 
 @pytest.mark.parametrize("env", [
-    {"LFBP_STAGE_MAX_KB": "4"},            # forces the i-chunked path
-    {"LFBP_STAGES": "1"}, {"LFBP_STAGES": "2", "LFBP_THREADS": "64"},
+    {"LFBP_STAGE_MAX_KB": "2"},            # forces the i-chunked path
+    {"LFBP_STAGES": "1"}, {"LFBP_STAGES": "2", "LFBP_CONSUMER_WARPS": "1"},
     {"LFBP_STAGE_KB": "1"}, {"LFBP_STAGE_KB": "200", "LFBP_STAGE_MAX_KB": "200"},
-    {"LFBP_CTAS_PER_SM": "1", "LFBP_THREADS": "512"}, {"LFBP_BAND": "3"},
+    {"LFBP_CTAS_PER_SM": "1", "LFBP_CONSUMER_WARPS": "16"}, {"LFBP_BAND": "3"},
 ])
 @pytest.mark.parametrize("shape,dtype", [((55, 55, 11, 11, 2), np.float32), ((27, 20, 13, 5, 2), np.float64),
                                          ((66, 41, 21, 9, 1), np.float32)])
@@ -157,7 +157,7 @@ def test_plan_variants_are_bit_exact(monkeypatch, env, shape, dtype):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     p = plan(shape, dtype)
-    if env.get("LFBP_STAGE_MAX_KB") == "4":
+    if env.get("LFBP_STAGE_MAX_KB") == "2":
         assert p["n_chunks"] > 1
     H = random_psf_like_reference(shape, density=0.9, seed=7, dtype=dtype)
     out = hprime_device(to_device(H))

@@ -81,10 +81,13 @@ def test_plans_for_every_config_fit_b200(cfg):
     assert p["smem_bytes"] <= 232448
     assert p["stages"] >= 2 and p["grid"] >= 148
     assert p["n_units"] < 2 ** 31
-    assert p["row_pitch"] % 16 == 0
-    # one staged unit holds J full rows per x (or an i-chunk)
-    n_s = w.shape[0]
-    assert p["row_pitch"] >= min(p["J"] * n_s, p["C"]) * w.itemsize + 16
+    # pitch is congruent to the x-stride mod 16 (linear smem addressing over x)
+    n_s, n_t = w.shape[:2]
+    assert p["row_pitch"] % 16 == (n_s * n_t * w.itemsize) % 16
+    # one staged unit holds J full rows per x (or an i-chunk) plus alignment slack
+    run = (p["J"] * n_s if p["n_chunks"] == 1 else p["C"]) * w.itemsize
+    assert p["row_pitch"] >= run + 32
+    assert p["stage_bytes"] >= w.shape[2] * p["row_pitch"] + 32
 
 
 def test_plan_chunks_huge_slabs():

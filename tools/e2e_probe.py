@@ -1,0 +1,89 @@
+"""Host-path probe on the GPU box: drop-in / C-ABI host-to-host timings.
+
+    python tools/e2e_probe.py [--config C2]
+
+Times (wall clock, synchronous calls): the pinned-buffer C-ABI path at
+several chunk sizes, the drop-in ``compute_backprojection`` on a pageable
+numpy array with and without per-call host registration, and checks every
+result against the device path's bytes.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import hashlib
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+
+    from paper_2003_09133_b200 import Dims5, PsfArray, _native, compute_backprojection
+    from paper_2003_09133_b200.configs import WORKLOADS
+    from paper_2003_09133_b200.synth import baseline_psf
+    w = WORKLOADS[a.config]
+    tdt = torch.float32 if w.itemsize == 4 else torch.float64
+    pin_in = torch.empty(w.n_elems, dtype=tdt, pin_memory=True)
+    pin_out = torch.empty(w.n_elems, dtype=tdt, pin_memory=True)
+    H = pin_in.numpy().reshape(w.shape, order="F")
+    baseline_psf(w, out=H)
+    code = _native.F32 if w.itemsize == 4 else _native.F64
+    dvec = _native.dims_array(w.shape)
+    step_bytes = 2 * w.nbytes
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(a.reps):
+            t = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t)
+        return min(ts), sorted(ts)[len(ts) // 2]
+
+    ref = None
+    for mb in (16, 32, 64, 128, 256):
+        os.environ["LFBP_CHUNK_MB"] = str(mb)
+
+        def call():
+            _native.check(_native.lib().lfbp_hprime_host(ctypes.c_void_p(pin_in.data_ptr()),
+                                                         ctypes.c_void_p(pin_out.data_ptr()), dvec, code, 0, 0, 0))
+        best, med = timed(call)
+        dig = hashlib.sha256(pin_out.numpy().tobytes()).hexdigest()
+        ref = ref or dig
+        print(json.dumps({"path": "c-abi pinned", "chunk_mb": mb, "best_ms": round(best * 1e3, 2),
+                          "med_ms": round(med * 1e3, 2), "GBps_rw": round(step_bytes / best / 1e9, 2),
+                          "same": dig == ref}), flush=True)
+    os.environ.pop("LFBP_CHUNK_MB", None)
+    pageable = np.array(H, order="F")
+    pageable.flags.writeable = False
+    psf = PsfArray._wrap(Dims5(*w.shape), pageable)
+    for reg in (True, False):
+        if reg:
+            os.environ.pop("LFBP_NO_HOST_REGISTER", None)
+        else:
+            os.environ["LFBP_NO_HOST_REGISTER"] = "1"
+        out = {}
+
+        def dropin():
+            out["bp"] = compute_backprojection(psf)
+        best, med = timed(dropin)
+        dig = hashlib.sha256(out["bp"].data.tobytes(order="F")).hexdigest()
+        print(json.dumps({"path": "drop-in pageable input", "host_register": reg, "best_ms": round(best * 1e3, 2),
+                          "med_ms": round(med * 1e3, 2), "GBps_rw": round(step_bytes / best / 1e9, 2),
+                          "same": dig == ref}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
