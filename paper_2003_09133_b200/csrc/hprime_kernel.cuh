@@ -78,6 +78,14 @@ __device__ __forceinline__ void st_v2_64_na(void* p, unsigned long long a, unsig
   asm volatile("st.global.L1::no_allocate.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
+// Decoded unit, written by the producer at the head of its stage so the
+// consumer warps read it with a few LDS instead of re-decoding.
+struct UnitHdr {
+  long long plane_off;  // z * plane_elems
+  int32_t y, t0, jb, i_lo, i_hi, s_lo, o0, pad;
+};
+constexpr int kHdrBytes = 64;
+
 struct Unit {
   int64_t z, y;
   int32_t t0, jb;        // band start and rows
@@ -153,7 +161,7 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
       if (a_hi > lim) a_hi = lim > a_lo ? lim : a_lo;
       // element k of run x lives at R0 + x*row_pitch + k*E (see hprime_plan.h);
       // its 16-byte aligned superset starts (b & 15) bytes earlier
-      uint8_t* dst = stage + 16 + (b0 & 15) + static_cast<int64_t>(x) * p.row_pitch - (b & 15);
+      uint8_t* dst = stage + kHdrBytes + 16 + (b0 & 15) + static_cast<int64_t>(x) * p.row_pitch - (b & 15);
       if (a_hi > a_lo) {
         const uint32_t n = static_cast<uint32_t>(a_hi - a_lo);
         if (p.flags & HP_FLAG_LOAD_EVICT_FIRST)
@@ -167,8 +175,19 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
         *reinterpret_cast<T*>(dst + (q - a_lo)) = *reinterpret_cast<const T*>(src + q);
     }
   }
+  if (lane == 0) {
+    UnitHdr* h = reinterpret_cast<UnitHdr*>(stage);
+    h->plane_off = w.z * (p.n_s * p.n_t * p.n_x * p.n_y);
+    h->y = static_cast<int32_t>(w.y);
+    h->t0 = w.t0;
+    h->jb = w.jb;
+    h->i_lo = w.i_lo;
+    h->i_hi = w.i_hi;
+    h->s_lo = w.s_lo;
+    h->o0 = static_cast<int32_t>(b0 & 15);
+  }
   tx = __reduce_add_sync(0xffffffffu, tx);
-  __syncwarp();                                    // tail stores before the release
+  __syncwarp();                                    // header and tail stores before the release
   if (lane == 0) mbar_arrive_expect_tx(bar, tx);  // tx-count may be transiently negative: legal
 }
 
@@ -185,76 +204,135 @@ __device__ __forceinline__ typename Word<E>::T lds(uint32_t addr) {
   }
 }
 
-// Consumer warps (cw of nc) write the J * n_x output rows of unit `u`.
 template <int E>
-__device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restrict__ dst, uint32_t u,
+__device__ __forceinline__ void st_vec(typename Word<E>::T* dst, const typename Word<E>::T* v) {
+  if constexpr (E == 4)
+    st_v4(dst, v[0], v[1], v[2], v[3]);
+  else
+    st_v2_64(dst, v[0], v[1]);
+}
+
+// Values of the VE elements of group g whose first element has source phase
+// x0 and smem address a0, for any n_x (general wrap); used for row edges and
+// for n_x < VE.
+template <int E>
+__device__ __forceinline__ void load_group_general(typename Word<E>::T* v, uint32_t a0, uint32_t x0, int32_t n_x,
+                                                   int32_t step, int32_t nr) {
+  constexpr int VE = 16 / E;
+  uint32_t a = a0, x = x0;
+#pragma unroll
+  for (int q = 0; q < VE; ++q) {
+    v[q] = lds<E>(a);
+    const bool last = x == static_cast<uint32_t>(n_x - 1);
+    a += last ? step - nr : step;
+    x = last ? 0u : x + 1;
+  }
+}
+
+// Consumer warps (cw of nc) write the J * n_x output rows of the unit staged
+// at `stage` (smem address `stage_s`).  A row is cut on the 16-byte grid of
+// H' into groups of VE = 16/E elements; the (at most two) partial edge groups
+// are written with masked scalar stores by lanes 0 and 1, the full groups by
+// all lanes, one st.global.v4 each, in a loop with no per-element branches:
+// stepping i -> i+1 moves the smem address by rp - E, minus n_x*rp when the
+// source phase x wraps (at most once per group when n_x >= VE).
+template <int E>
+__device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restrict__ dst, const uint8_t* stage,
                                              uint32_t stage_s, int cw, int nc, int lane) {
   using T = typename Word<E>::T;
   constexpr int VE = 16 / E;
-  const Unit w = decode_unit(p, u);
+  const UnitHdr h = *reinterpret_cast<const UnitHdr*>(stage);
   const int32_t n_x = static_cast<int32_t>(p.n_x);
+  const int32_t n_s = static_cast<int32_t>(p.n_s);
   const int32_t rp = p.row_pitch;
-  const uint32_t base = stage_s + 16 + static_cast<uint32_t>((w.run_off0 * E) & 15);
   const int32_t step = rp - E;                    // x -> x+1, s -> s-1
-  const int32_t wrap = step - n_x * rp;           // ... and x wraps to 0
-  const int32_t i_end = min(w.i_hi, p.v_s);       // loaded elements: [i_lo, i_end)
-  const int64_t xs = p.n_s * p.n_t;               // element stride of x'
-  const int32_t rows = w.jb * n_x;
-  for (int32_t r = cw; r < rows; r += nc) {
-    const int32_t tl = static_cast<int32_t>(hp_div(p.nx_div, static_cast<uint32_t>(r)));
-    const int32_t xp = r - tl * n_x;
-    const int32_t t = w.t0 + tl;
+  const int32_t nr = n_x * rp;                    // ... minus this when x wraps to 0
+  const uint32_t base = stage_s + kHdrBytes + 16 + static_cast<uint32_t>(h.o0);
+  const int32_t i_end = min(h.i_hi, p.v_s);       // loaded elements: [i_lo, i_end)
+  const int32_t xs = n_s * static_cast<int32_t>(p.n_t);   // in-plane offsets are 32-bit
+  const int32_t zmis = static_cast<int32_t>(h.plane_off & (VE - 1));
+  const uint32_t inc_x = static_cast<uint32_t>(p.gx_inc);              // (32*VE) mod n_x
+  const int32_t inc_a = p.gx_inc * rp - 32 * VE * E;                   // smem step of 32 groups
+  T* dz = reinterpret_cast<T*>(dst) + h.plane_off;
+  int32_t tl = 0, xp = cw;
+  while (xp >= n_x) {
+    xp -= n_x;
+    ++tl;
+  }
+  while (tl < h.jb) {
+    const int32_t t = h.t0 + tl;
     const bool zero_row = t >= p.v_t;  // dropped source row t = n_t - 1 (even n_t)
-    const int64_t j = zero_row ? p.n_t - 1 : 2 * p.c_t - t;
-    const int64_t yp = zero_row ? w.y : hp_mod(p.ny_div, static_cast<uint32_t>(w.y + t + p.ny_off));
-    const int64_t O = p.n_s * j + xs * (xp + p.n_x * (yp + p.n_y * w.z));
-    T* orow = reinterpret_cast<T*>(dst) + O;
+    const int32_t j = zero_row ? static_cast<int32_t>(p.n_t) - 1 : 2 * p.c_t - t;
+    const int32_t yp = zero_row ? h.y : static_cast<int32_t>(hp_mod(p.ny_div, static_cast<uint32_t>(h.y + t + p.ny_off)));
+    const int32_t o_in = n_s * j + xs * (xp + n_x * yp);
+    T* orow = dz + o_in;
     if (zero_row) {
-      for (int32_t i = w.i_lo + lane; i < w.i_hi; i += 32) orow[i] = T(0);
-      continue;
-    }
-    if (i_end < w.i_hi && lane == 0) orow[p.n_s - 1] = T(0);  // even n_s: row i = n_s - 1 is zero
-    // element address of (x, i): base + x*rp + (tl*n_s - s_lo + 2c_s - i)*E
-    const int32_t k0 = tl * static_cast<int32_t>(p.n_s) - w.s_lo + 2 * p.c_s;
-    auto addr_of = [&](int32_t i, uint32_t& x) -> uint32_t {
-      x = hp_mod(p.nx_div, static_cast<uint32_t>(xp + i + p.nx_off));
-      return base + x * rp + (k0 - i) * E;
-    };
-    // head / body / tail split on the 16-byte grid of the output row
-    const int32_t mis = static_cast<int32_t>((O + w.i_lo) & (VE - 1));
-    const int32_t head = max(0, min(mis ? VE - mis : 0, i_end - w.i_lo));
-    const int32_t b0 = w.i_lo + head;
-    const int32_t nb = max(0, (i_end - b0) / VE);
-    const int32_t b1 = b0 + nb * VE;
-    // scalar head and tail (< VE elements each)
-    if (lane < head || (lane >= VE && lane - VE < i_end - b1)) {
-      const int32_t i = lane < head ? w.i_lo + lane : b1 + lane - VE;
-      uint32_t x;
-      orow[i] = lds<E>(addr_of(i, x));
-    }
-    for (int32_t g = lane; g < nb; g += 32) {
-      const int32_t i0 = b0 + g * VE;
-      uint32_t x;
-      uint32_t a = addr_of(i0, x);
-      T v[VE];
+      for (int32_t i = h.i_lo + lane; i < h.i_hi; i += 32) orow[i] = T(0);
+    } else if (i_end > h.i_lo) {
+      const int32_t mis = (o_in + zmis + h.i_lo) & (VE - 1);
+      const int32_t gs = h.i_lo - mis;                        // first group start (element i)
+      const int32_t ng = (i_end - gs + VE - 1) / VE;
+      const bool last_full = ((i_end - gs) & (VE - 1)) == 0;
+      const int32_t gf0 = mis ? 1 : 0;                        // full groups [gf0, gf1)
+      const int32_t gf1 = last_full ? ng : ng - 1;
+      // smem address of (x, i) = base + x*rp + (tl*n_s - s_lo + 2c_s - i)*E
+      const uint32_t a_row = base + static_cast<uint32_t>((tl * n_s - h.s_lo + 2 * p.c_s - gs) * E);
+      const uint32_t xoff = static_cast<uint32_t>(xp + gs + p.nx_off + VE * n_x);
+      T* og = orow + gs;
+      // partial edge groups: lane 0 the first, lane 1 the last
+      if (lane < 2) {
+        const int32_t g = lane == 0 ? 0 : ng - 1;
+        const bool partial = lane == 0 ? (mis != 0 || (ng == 1 && !last_full)) : (!last_full && ng > 1);
+        if (partial) {
+          const uint32_t x0 = hp_mod(p.nx_div, xoff + g * VE);
+          T v[VE];
+          load_group_general<E>(v, a_row + x0 * rp - g * (VE * E), x0, n_x, step, nr);
 #pragma unroll
-      for (int q = 0; q < VE; ++q) {
-        v[q] = lds<E>(a);
-        const bool last = x == static_cast<uint32_t>(n_x - 1);
-        a += last ? wrap : step;
-        x = last ? 0u : x + 1;
+          for (int q = 0; q < VE; ++q) {
+            const int32_t i = gs + g * VE + q;
+            if (i >= h.i_lo && i < i_end) og[g * VE + q] = v[q];
+          }
+        }
       }
-      if (p.flags & HP_FLAG_STORE_NA) {
-        if constexpr (E == 4)
-          st_v4_na(orow + i0, v[0], v[1], v[2], v[3]);
-        else
-          st_v2_64_na(orow + i0, v[0], v[1]);
-      } else {
-        if constexpr (E == 4)
-          st_v4(orow + i0, v[0], v[1], v[2], v[3]);
-        else
-          st_v2_64(orow + i0, v[0], v[1]);
+      if (i_end < h.i_hi && lane == 0) orow[n_s - 1] = T(0);  // even n_s: row i = n_s - 1 is zero
+      int32_t g = gf0 + lane;
+      if (g < gf1) {
+        uint32_t x0 = hp_mod(p.nx_div, xoff + g * VE);
+        uint32_t a0 = a_row + x0 * rp - g * (VE * E);
+        T* o = og + g * VE;
+        if (n_x >= VE) {  // at most one wrap inside a group
+          for (; g < gf1; g += 32) {
+            const int32_t d = n_x - static_cast<int32_t>(x0);
+            const uint32_t aw = a0 - nr;
+            T v[VE];
+            v[0] = lds<E>(a0);
+#pragma unroll
+            for (int q = 1; q < VE; ++q) v[q] = lds<E>((q >= d ? aw : a0) + q * step);
+            st_vec<E>(o, v);
+            o += 32 * VE;
+            x0 += inc_x;
+            a0 += inc_a;
+            if (x0 >= static_cast<uint32_t>(n_x)) {
+              x0 -= n_x;
+              a0 -= nr;
+            }
+          }
+        } else {
+          for (; g < gf1; g += 32) {
+            T v[VE];
+            load_group_general<E>(v, a0, x0, n_x, step, nr);
+            st_vec<E>(o, v);
+            o += 32 * VE;
+            x0 = hp_mod(p.nx_div, xoff + (g + 32) * VE);
+            a0 = a_row + x0 * rp - (g + 32) * (VE * E);
+          }
+        }
       }
+    }
+    xp += nc;
+    while (xp >= n_x) {
+      xp -= n_x;
+      ++tl;
     }
   }
 }
@@ -306,8 +384,8 @@ __global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8
   uint32_t ph = 0;
   for (uint32_t k = 0; k < mine; ++k) {
     mbar_wait(smem_u32(&full[st]), ph);
-    consume_unit<E>(p, dst, first + k * stride, stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - 1, nc,
-                    lane);
+    consume_unit<E>(p, dst, stages + static_cast<int64_t>(st) * p.stage_bytes,
+                    stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - 1, nc, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     if (++st == S) {

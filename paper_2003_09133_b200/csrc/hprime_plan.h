@@ -16,9 +16,9 @@
 // H'[i_lo:i_hi, j, x', y', z] with j = 2c_t - t and
 // y' = (y + t - c_t) mod n_y, written with 16-byte stores.
 //
-// Shared-memory layout of one stage: element k of the run of source phase x
-// sits at byte  R0 + x * row_pitch + k * elem,  R0 = 16 + (run byte offset
-// mod 16).  row_pitch is congruent to (n_s * n_t * elem) mod 16, so every
+// Shared-memory layout of one stage: a 64-byte unit header, then element k
+// of the run of source phase x at byte  R0 + x * row_pitch + k * elem,
+// R0 = 64 + 16 + (run byte offset mod 16).  row_pitch is congruent to (n_s * n_t * elem) mod 16, so every
 // run's 16-byte-aligned superset lands on a 16-byte-aligned smem address (a
 // legal bulk-copy destination) while the element address stays LINEAR in x:
 // the consumer steps x -> x+1, s -> s-1 with one add.
@@ -64,7 +64,6 @@ HP_HD uint32_t hp_mod(const HpFastDiv& f, uint32_t n) {
 }
 
 #define HP_FLAG_LOAD_EVICT_FIRST 1  // L2 evict_first hint on the bulk loads of H
-#define HP_FLAG_STORE_NA 2          // st.global.L1::no_allocate for H'
 
 struct HpPlan {
   // geometry of the (chunk) arrays the kernel sees
@@ -89,6 +88,7 @@ struct HpPlan {
   int32_t ctas_per_sm;
   int32_t xs16;               // (n_s * n_t * elem) mod 16: run misalignment step per x
   int32_t flags;              // HP_FLAG_*
+  int32_t gx_inc;             // (32 * 16/elem) mod n_x: phase advance of one 32-group stride
   int64_t n_units;            // z_count * n_chunks * n_bands * n_y  (< 2^31)
   HpFastDiv nx_div;           // mod n_x on the element path
   HpFastDiv ny_div;           // unit decode / y' wrap

@@ -111,8 +111,9 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   p.nx_off = static_cast<int32_t>((d[2] - (p.c_s % d[2])) % d[2]);
   p.ny_off = static_cast<int32_t>((d[3] - (p.c_t % d[3])) % d[3]);
   p.xs16 = static_cast<int32_t>((d[0] * d[1] * E) & 15);
-  if (d[0] >= (1ll << 30) || d[1] >= (1ll << 30) || d[2] >= (1 << 20) || d[3] >= (1 << 20))
-    return fail(LFBP_ERR_UNSUPPORTED, "axis too long for the kernel's 32-bit in-plane indices");
+  if (d[0] * d[1] * d[2] * d[3] >= (1ll << 31) || d[2] >= (1 << 20) || d[3] >= (1 << 20))
+    return fail(LFBP_ERR_UNSUPPORTED, "depth plane of %lld elements exceeds the kernel's 32-bit in-plane offsets",
+                (long long)(d[0] * d[1] * d[2] * d[3]));
 
   const int64_t stage_target = int64_t(env_int("LFBP_STAGE_KB", 32)) * 1024;
   const int64_t stage_max = int64_t(env_int("LFBP_STAGE_MAX_KB", 100)) * 1024;
@@ -142,8 +143,8 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   if (((pitch / 16) & 1) == 0) pitch += 16;
   pitch += env_int("LFBP_PITCH_EXTRA16", 0) * 16;
   p.row_pitch = static_cast<int32_t>(pitch + p.xs16);
-  p.stage_bytes = static_cast<int32_t>(round_up(d[2] * p.row_pitch + 32, 128));
-  int S = env_int("LFBP_STAGES", 4);
+  p.stage_bytes = static_cast<int32_t>(round_up(64 + d[2] * p.row_pitch + 32, 128));  // header + runs
+  int S = env_int("LFBP_STAGES", 3);
   S = std::max(1, std::min(S, 8));
   while (S > 1 && 128 + int64_t(S) * p.stage_bytes > dp.smem_optin) --S;
   if (128 + int64_t(S) * p.stage_bytes > dp.smem_optin)
@@ -175,6 +176,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   p.ctas_per_sm = per_sm;
   p.grid = static_cast<int32_t>(std::min<int64_t>(units, int64_t(per_sm) * dp.sm_count));
   p.flags = env_int("LFBP_KFLAGS", 0);
+  p.gx_inc = static_cast<int32_t>((32 * (16 / E)) % d[2]);
   p.nx_div = hp_fastdiv_make(static_cast<uint32_t>(d[2]));
   p.ny_div = hp_fastdiv_make(static_cast<uint32_t>(d[3]));
   p.nb_div = hp_fastdiv_make(static_cast<uint32_t>(p.n_bands));

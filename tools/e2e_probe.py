@@ -52,6 +52,33 @@ def main():
             ts.append(time.perf_counter() - t)
         return min(ts), sorted(ts)[len(ts) // 2]
 
+    # PCIe ceilings: H2D alone, D2H alone, both at once (separate streams)
+    dev_a = torch.empty(w.n_elems, dtype=tdt, device="cuda")
+    dev_b = torch.empty(w.n_elems, dtype=tdt, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            dev_a.copy_(pin_in, non_blocking=True)
+        s1.synchronize()
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            pin_out.copy_(dev_b, non_blocking=True)
+        s2.synchronize()
+
+    def both():
+        with torch.cuda.stream(s1):
+            dev_a.copy_(pin_in, non_blocking=True)
+        with torch.cuda.stream(s2):
+            pin_out.copy_(dev_b, non_blocking=True)
+        s1.synchronize()
+        s2.synchronize()
+    for name, fn, nb in (("h2d", h2d, w.nbytes), ("d2h", d2h, w.nbytes), ("h2d+d2h", both, 2 * w.nbytes)):
+        best, med = timed(fn)
+        print(json.dumps({"path": "pcie " + name, "best_ms": round(best * 1e3, 2), "GBps": round(nb / best / 1e9, 2)}),
+              flush=True)
+    del dev_a, dev_b
     ref = None
     for mb in (16, 32, 64, 128, 256):
         os.environ["LFBP_CHUNK_MB"] = str(mb)
