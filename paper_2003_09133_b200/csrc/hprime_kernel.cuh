@@ -230,12 +230,16 @@ __device__ __forceinline__ void load_group_general(typename Word<E>::T* v, uint3
 }
 
 // Consumer warps (cw of nc) write the J * n_x output rows of the unit staged
-// at `stage` (smem address `stage_s`).  A row is cut on the 16-byte grid of
-// H' into groups of VE = 16/E elements; the (at most two) partial edge groups
-// are written with masked scalar stores by lanes 0 and 1, the full groups by
-// all lanes, one st.global.v4 each, in a loop with no per-element branches:
-// stepping i -> i+1 moves the smem address by rp - E, minus n_x*rp when the
-// source phase x wraps (at most once per group when n_x >= VE).
+// at `stage` (smem address `stage_s`).  Each warp is split into 32/W
+// sub-warps of W lanes (W = p.sub_width); a sub-warp owns one output row at a
+// time, so the per-row index arithmetic is shared by 32/W rows and every
+// store instruction still writes W*16 contiguous bytes per row.  A row is cut
+// on the 16-byte grid of H' into groups of VE = 16/E elements; lane l of the
+// sub-warp takes groups l, l+W, ...  Full groups are one st.global.v4; the
+// (at most two) partial edge groups use predicated scalar stores.  Stepping
+// i -> i+1 moves the smem address by rp - E, minus n_x*rp when the source
+// phase x wraps (at most once per group when n_x >= VE): no divisions in the
+// element loop.
 template <int E>
 __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restrict__ dst, const uint8_t* stage,
                                              uint32_t stage_s, int cw, int nc, int lane) {
@@ -244,17 +248,23 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
   const UnitHdr h = *reinterpret_cast<const UnitHdr*>(stage);
   const int32_t n_x = static_cast<int32_t>(p.n_x);
   const int32_t n_s = static_cast<int32_t>(p.n_s);
+  const int32_t W = p.sub_width;
+  const int32_t sl = lane & (W - 1);               // lane within the sub-warp
+  const int32_t R = 32 / W;                        // rows in flight per warp
   const int32_t rp = p.row_pitch;
-  const int32_t step = rp - E;                    // x -> x+1, s -> s-1
-  const int32_t nr = n_x * rp;                    // ... minus this when x wraps to 0
+  const int32_t step = rp - E;                     // x -> x+1, s -> s-1
+  const int32_t nr = n_x * rp;                     // ... minus this when x wraps to 0
   const uint32_t base = stage_s + kHdrBytes + 16 + static_cast<uint32_t>(h.o0);
-  const int32_t i_end = min(h.i_hi, p.v_s);       // loaded elements: [i_lo, i_end)
+  const int32_t i_lo = h.i_lo;
+  const int32_t i_end = min(h.i_hi, p.v_s);        // loaded elements: [i_lo, i_end)
   const int32_t xs = n_s * static_cast<int32_t>(p.n_t);   // in-plane offsets are 32-bit
   const int32_t zmis = static_cast<int32_t>(h.plane_off & (VE - 1));
-  const uint32_t inc_x = static_cast<uint32_t>(p.gx_inc);              // (32*VE) mod n_x
-  const int32_t inc_a = p.gx_inc * rp - 32 * VE * E;                   // smem step of 32 groups
+  const uint32_t inc_x = static_cast<uint32_t>(p.gx_inc);              // (W*VE) mod n_x
+  const int32_t inc_a = p.gx_inc * rp - W * VE * E;                    // smem step of W groups
+  const bool wrap1 = n_x >= VE;
+  const int32_t rstep = nc * R;
   T* dz = reinterpret_cast<T*>(dst) + h.plane_off;
-  int32_t tl = 0, xp = cw;
+  int32_t tl = 0, xp = cw * R + lane / W;
   while (xp >= n_x) {
     xp -= n_x;
     ++tl;
@@ -267,69 +277,48 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
     const int32_t o_in = n_s * j + xs * (xp + n_x * yp);
     T* orow = dz + o_in;
     if (zero_row) {
-      for (int32_t i = h.i_lo + lane; i < h.i_hi; i += 32) orow[i] = T(0);
-    } else if (i_end > h.i_lo) {
-      const int32_t mis = (o_in + zmis + h.i_lo) & (VE - 1);
-      const int32_t gs = h.i_lo - mis;                        // first group start (element i)
-      const int32_t ng = (i_end - gs + VE - 1) / VE;
-      const bool last_full = ((i_end - gs) & (VE - 1)) == 0;
-      const int32_t gf0 = mis ? 1 : 0;                        // full groups [gf0, gf1)
-      const int32_t gf1 = last_full ? ng : ng - 1;
-      // smem address of (x, i) = base + x*rp + (tl*n_s - s_lo + 2c_s - i)*E
-      const uint32_t a_row = base + static_cast<uint32_t>((tl * n_s - h.s_lo + 2 * p.c_s - gs) * E);
-      const uint32_t xoff = static_cast<uint32_t>(xp + gs + p.nx_off + VE * n_x);
-      T* og = orow + gs;
-      // partial edge groups: lane 0 the first, lane 1 the last
-      if (lane < 2) {
-        const int32_t g = lane == 0 ? 0 : ng - 1;
-        const bool partial = lane == 0 ? (mis != 0 || (ng == 1 && !last_full)) : (!last_full && ng > 1);
-        if (partial) {
-          const uint32_t x0 = hp_mod(p.nx_div, xoff + g * VE);
+      for (int32_t i = i_lo + sl; i < h.i_hi; i += W) orow[i] = T(0);
+    } else {
+      if (i_end < h.i_hi && sl == 0) orow[n_s - 1] = T(0);  // even n_s: row i = n_s - 1 is zero
+      const int32_t gs = i_lo - ((o_in + zmis + i_lo) & (VE - 1));   // first group start (element i)
+      const int32_t ng = i_end > i_lo ? (i_end - gs + VE - 1) / VE : 0;
+      int32_t g = sl;
+      if (g < ng) {
+        // smem address of (x, i) = base + x*rp + (tl*n_s - s_lo + 2c_s - i)*E
+        uint32_t x0 = hp_mod(p.nx_div, static_cast<uint32_t>(xp + gs + p.nx_off + VE * n_x + g * VE));
+        uint32_t a0 = base + static_cast<uint32_t>((tl * n_s - h.s_lo + 2 * p.c_s - gs - g * VE) * E) + x0 * rp;
+        int32_t i0 = gs + g * VE;
+        T* o = orow + i0;
+        for (; g < ng; g += W) {
           T v[VE];
-          load_group_general<E>(v, a_row + x0 * rp - g * (VE * E), x0, n_x, step, nr);
-#pragma unroll
-          for (int q = 0; q < VE; ++q) {
-            const int32_t i = gs + g * VE + q;
-            if (i >= h.i_lo && i < i_end) og[g * VE + q] = v[q];
-          }
-        }
-      }
-      if (i_end < h.i_hi && lane == 0) orow[n_s - 1] = T(0);  // even n_s: row i = n_s - 1 is zero
-      int32_t g = gf0 + lane;
-      if (g < gf1) {
-        uint32_t x0 = hp_mod(p.nx_div, xoff + g * VE);
-        uint32_t a0 = a_row + x0 * rp - g * (VE * E);
-        T* o = og + g * VE;
-        if (n_x >= VE) {  // at most one wrap inside a group
-          for (; g < gf1; g += 32) {
+          if (wrap1) {  // at most one wrap inside a group
             const int32_t d = n_x - static_cast<int32_t>(x0);
             const uint32_t aw = a0 - nr;
-            T v[VE];
             v[0] = lds<E>(a0);
 #pragma unroll
             for (int q = 1; q < VE; ++q) v[q] = lds<E>((q >= d ? aw : a0) + q * step);
-            st_vec<E>(o, v);
-            o += 32 * VE;
-            x0 += inc_x;
-            a0 += inc_a;
-            if (x0 >= static_cast<uint32_t>(n_x)) {
-              x0 -= n_x;
-              a0 -= nr;
-            }
-          }
-        } else {
-          for (; g < gf1; g += 32) {
-            T v[VE];
+          } else {
             load_group_general<E>(v, a0, x0, n_x, step, nr);
+          }
+          if (i0 >= i_lo && i0 + VE <= i_end) {
             st_vec<E>(o, v);
-            o += 32 * VE;
-            x0 = hp_mod(p.nx_div, xoff + (g + 32) * VE);
-            a0 = a_row + x0 * rp - (g + 32) * (VE * E);
+          } else {
+#pragma unroll
+            for (int q = 0; q < VE; ++q)
+              if (i0 + q >= i_lo && i0 + q < i_end) o[q] = v[q];
+          }
+          o += W * VE;
+          i0 += W * VE;
+          x0 += inc_x;
+          a0 += inc_a;
+          if (x0 >= static_cast<uint32_t>(n_x)) {
+            x0 -= n_x;
+            a0 -= nr;
           }
         }
       }
     }
-    xp += nc;
+    xp += rstep;
     while (xp >= n_x) {
       xp -= n_x;
       ++tl;

@@ -91,9 +91,36 @@ int elem_size(int dtype) { return dtype == LFBP_F32 ? 4 : dtype == LFBP_F64 ? 8 
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+// Tunable launch knobs.  Environment variables (LFBP_STAGES, LFBP_STAGE_KB,
+// LFBP_CONSUMER_WARPS, LFBP_SUBWARP) override them for sweeps and tests.
+struct Knobs {
+  int stages = 3;      // smem ring depth
+  int stage_kb = 48;   // target bytes of one staged unit (sets the t-band J)
+  int cwarps = 12;     // consumer warps per CTA
+  int subwarp = 0;     // lanes per output row; 0 = by row length
+};
+
+const char* const kKnobEnv[] = {"LFBP_STAGES", "LFBP_STAGE_KB", "LFBP_CONSUMER_WARPS", "LFBP_SUBWARP",
+                                "LFBP_CTAS_PER_SM", "LFBP_BAND", "LFBP_STAGE_MAX_KB"};
+
+bool env_knobs_set() {
+  for (const char* n : kKnobEnv) {
+    const char* v = getenv(n);
+    if (v && *v) return true;
+  }
+  return false;
+}
+
+// Candidates tried by the autotuner (measured best plans of C1..C5 and
+// neighbours; every one is bit-exact, they differ only in speed).
+const Knobs kCandidates[] = {
+    {3, 48, 12, 8}, {4, 48, 12, 16}, {3, 16, 4, 16}, {3, 32, 8, 16},
+    {2, 16, 8, 8},  {3, 16, 6, 32},  {2, 32, 4, 8},  {4, 32, 8, 16},
+};
+
 // Work-unit shape, smem ring and persistent grid for one launch.
 int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_count,
-              int64_t total_bytes, int dev) {
+              int64_t total_bytes, int dev, const Knobs& kn = Knobs()) {
   memset(&p, 0, sizeof(p));
   const DevProps dp = device_props(dev);
   p.n_s = d[0];
@@ -115,7 +142,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
     return fail(LFBP_ERR_UNSUPPORTED, "depth plane of %lld elements exceeds the kernel's 32-bit in-plane offsets",
                 (long long)(d[0] * d[1] * d[2] * d[3]));
 
-  const int64_t stage_target = int64_t(env_int("LFBP_STAGE_KB", 32)) * 1024;
+  const int64_t stage_target = int64_t(env_int("LFBP_STAGE_KB", kn.stage_kb)) * 1024;
   const int64_t stage_max = int64_t(env_int("LFBP_STAGE_MAX_KB", 100)) * 1024;
   const int64_t row_full = d[0] * E;
   int64_t run_max;
@@ -144,15 +171,15 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   pitch += env_int("LFBP_PITCH_EXTRA16", 0) * 16;
   p.row_pitch = static_cast<int32_t>(pitch + p.xs16);
   p.stage_bytes = static_cast<int32_t>(round_up(64 + d[2] * p.row_pitch + 32, 128));  // header + runs
-  int S = env_int("LFBP_STAGES", 3);
+  int S = env_int("LFBP_STAGES", kn.stages);
   S = std::max(1, std::min(S, 8));
   while (S > 1 && 128 + int64_t(S) * p.stage_bytes > dp.smem_optin) --S;
   if (128 + int64_t(S) * p.stage_bytes > dp.smem_optin)
     return fail(LFBP_ERR_UNSUPPORTED, "stage of %d bytes exceeds shared memory", p.stage_bytes);
   p.stages = S;
   p.smem_bytes = 128 + S * p.stage_bytes;
-  int cwarps = env_int("LFBP_CONSUMER_WARPS", 0);
-  if (cwarps <= 0) cwarps = p.smem_bytes > dp.smem_optin / 2 ? 16 : 8;
+  int cwarps = env_int("LFBP_CONSUMER_WARPS", kn.cwarps);
+  if (cwarps <= 0) cwarps = 12;
   cwarps = std::max(1, std::min(16, cwarps));
   const int threads = 32 * (1 + cwarps);
   p.threads = threads;
@@ -176,7 +203,12 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   p.ctas_per_sm = per_sm;
   p.grid = static_cast<int32_t>(std::min<int64_t>(units, int64_t(per_sm) * dp.sm_count));
   p.flags = env_int("LFBP_KFLAGS", 0);
-  p.gx_inc = static_cast<int32_t>((32 * (16 / E)) % d[2]);
+  // lanes per output row: enough 16-byte groups per lane to amortise the row setup
+  const int64_t groups = (std::min<int64_t>(p.C, d[0]) * E + 15) / 16 + 1;
+  int W = env_int("LFBP_SUBWARP", kn.subwarp);
+  if (W != 8 && W != 16 && W != 32) W = groups <= 64 ? 8 : groups <= 128 ? 16 : 32;
+  p.sub_width = W;
+  p.gx_inc = static_cast<int32_t>((W * (16 / E)) % d[2]);
   p.nx_div = hp_fastdiv_make(static_cast<uint32_t>(d[2]));
   p.ny_div = hp_fastdiv_make(static_cast<uint32_t>(d[3]));
   p.nb_div = hp_fastdiv_make(static_cast<uint32_t>(p.n_bands));
@@ -194,6 +226,75 @@ int launch(const HpPlan& p, const void* src, void* dst, cudaStream_t st) {
                                                                    static_cast<uint8_t*>(dst));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   HP_CUDA(cudaGetLastError());
+  return LFBP_OK;
+}
+
+// ---- autotuner: per (plane shape, element size, device), first large call ----
+struct TuneKey {
+  int64_t n_s, n_t, n_x, n_y;
+  int E, dev;
+  bool operator<(const TuneKey& o) const {
+    if (n_s != o.n_s) return n_s < o.n_s;
+    if (n_t != o.n_t) return n_t < o.n_t;
+    if (n_x != o.n_x) return n_x < o.n_x;
+    if (n_y != o.n_y) return n_y < o.n_y;
+    if (E != o.E) return E < o.E;
+    return dev < o.dev;
+  }
+};
+
+std::mutex g_tune_mu;
+std::map<TuneKey, Knobs> g_tuned;
+
+bool tuned_knobs(const TuneKey& k, Knobs& out) {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  auto it = g_tuned.find(k);
+  if (it == g_tuned.end()) return false;
+  out = it->second;
+  return true;
+}
+
+// Time every candidate on the caller's buffers (the final launch overwrites
+// dst) and keep the fastest.  Skipped while the stream is being captured.
+int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[5], int E, int64_t z_begin,
+             int64_t z_count, int64_t total, cudaStream_t st, Knobs& best) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  HP_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return LFBP_OK;
+  cudaEvent_t e0, e1;
+  HP_CUDA(cudaEventCreate(&e0));
+  HP_CUDA(cudaEventCreate(&e1));
+  float best_ms = 1e30f;
+  bool found = false;
+  for (const Knobs& c : kCandidates) {
+    HpPlan p;
+    if (make_plan(p, dims, E, z_begin, z_count, total, key.dev, c) != LFBP_OK) continue;
+    int rc = launch(p, src, dst, st);
+    if (rc) return rc;
+    float ms = 1e30f;
+    for (int r = 0; r < 2; ++r) {
+      HP_CUDA(cudaEventRecord(e0, st));
+      rc = launch(p, src, dst, st);
+      if (rc) return rc;
+      HP_CUDA(cudaEventRecord(e1, st));
+      HP_CUDA(cudaEventSynchronize(e1));
+      float t = 0.f;
+      HP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+      ms = std::min(ms, t);
+    }
+    if (ms < best_ms) {
+      best_ms = ms;
+      best = c;
+      found = true;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  g_err.clear();
+  if (found) {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_tuned[key] = best;
+  }
   return LFBP_OK;
 }
 
@@ -322,8 +423,10 @@ int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, in
     HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.h2d_done[k], 0));
     if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.d2h_done[k], 0));  // out[k] drained
     int64_t cd[5] = {dims[0], dims[1], dims[2], dims[3], planes};
+    Knobs kn;
+    if (!env_knobs_set()) tuned_knobs(TuneKey{dims[0], dims[1], dims[2], dims[3], E, dev}, kn);
     HpPlan p;
-    rc = make_plan(p, cd, E, 0, planes, int64_t(bytes), dev);
+    rc = make_plan(p, cd, E, 0, planes, int64_t(bytes), dev, kn);
     if (rc) return rc;
     rc = launch(p, w.in[k], w.out[k], w.s_cmp);
     if (rc) return rc;
@@ -410,8 +513,17 @@ int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dt
   if (s8 < d8 + total && d8 < s8 + total) return fail(LFBP_ERR_ARGUMENT, "src and dst overlap");
   int dev = 0;
   HP_CUDA(cudaGetDevice(&dev));
+  Knobs kn;
+  if (!env_knobs_set()) {
+    const TuneKey key{dims[0], dims[1], dims[2], dims[3], E, dev};
+    const int64_t moved = 2 * plane_elems(dims) * (z_end - z_begin) * E;
+    if (!tuned_knobs(key, kn) && env_int("LFBP_AUTOTUNE", 1) && moved >= (int64_t(256) << 20)) {
+      rc = autotune(key, src, dst, dims, E, z_begin, z_end - z_begin, total, static_cast<cudaStream_t>(stream), kn);
+      if (rc) return rc;
+    }
+  }
   HpPlan p;
-  rc = make_plan(p, dims, E, z_begin, z_end - z_begin, total, dev);
+  rc = make_plan(p, dims, E, z_begin, z_end - z_begin, total, dev, kn);
   if (rc) return rc;
   return launch(p, src, dst, static_cast<cudaStream_t>(stream));
 }
@@ -513,17 +625,20 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
     cudaGetDevice(&dev);
   }
   const int E = elem_size(dtype);
+  Knobs kn;
+  const bool tuned = !env_knobs_set() && tuned_knobs(TuneKey{dims[0], dims[1], dims[2], dims[3], E, dev}, kn);
   HpPlan p;
-  rc = make_plan(p, dims, E, 0, dims[4], plane_elems(dims) * dims[4] * E, dev);
+  rc = make_plan(p, dims, E, 0, dims[4], plane_elems(dims) * dims[4] * E, dev, kn);
   if (rc) return rc;
   const DevProps dp = device_props(dev);
   int w = snprintf(buf, size_t(buf_len),
                    "{\"elem\": %d, \"J\": %d, \"n_bands\": %d, \"C\": %d, \"n_chunks\": %d, \"row_pitch\": %d, "
                    "\"stage_bytes\": %d, \"stages\": %d, \"threads\": %d, \"smem_bytes\": %d, \"ctas_per_sm\": %d, "
-                   "\"grid\": %d, \"n_units\": %lld, \"sm_count\": %d, \"device_props\": \"%s\"}",
+                   "\"grid\": %d, \"n_units\": %lld, \"sub_width\": %d, \"sm_count\": %d, \"device_props\": \"%s\", "
+                   "\"autotuned\": %s}",
                    p.elem, p.J, p.n_bands, p.C, p.n_chunks, p.row_pitch, p.stage_bytes, p.stages, p.threads,
-                   p.smem_bytes, p.ctas_per_sm, p.grid, (long long)p.n_units, dp.sm_count,
-                   dp.real ? "queried" : "b200-defaults");
+                   p.smem_bytes, p.ctas_per_sm, p.grid, (long long)p.n_units, p.sub_width, dp.sm_count,
+                   dp.real ? "queried" : "b200-defaults", tuned ? "true" : "false");
   if (w < 0 || w >= buf_len) return fail(LFBP_ERR_ARGUMENT, "buffer too small");
   return LFBP_OK;
 }

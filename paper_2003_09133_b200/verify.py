@@ -50,17 +50,30 @@ def first_mismatch_index(shape, byte_offset: int, itemsize: int) -> tuple[int, .
     return tuple(idx)
 
 
-def plane_digests(t, shape) -> list[str]:
-    """SHA-256 of each z-plane's bytes of a device tensor in F layout."""
+def plane_digests(t, shape, threads: int = 8) -> list[str]:
+    """SHA-256 of each z-plane's bytes of a device tensor in F layout.
+
+    Planes are copied to pinned host buffers in batches and hashed by a
+    thread pool (hashlib releases the GIL)."""
+    import concurrent.futures as cf
+
     import torch
     n_s, n_t, n_x, n_y, n_z = shape
     flat = t.reshape(-1) if t.is_contiguous() else t.permute(4, 3, 2, 1, 0).reshape(-1)
     per = n_s * n_t * n_x * n_y
-    host = torch.empty(per, dtype=t.dtype, pin_memory=True)
-    out = []
-    for z in range(n_z):
-        host.copy_(flat[z * per:(z + 1) * per])
-        out.append(hashlib.sha256(host.numpy().tobytes()).hexdigest())
+    batch = max(1, min(n_z, threads))
+    bufs = [torch.empty(per, dtype=t.dtype, pin_memory=True) for _ in range(batch)]
+    out = [None] * n_z
+
+    def digest(k, z):
+        out[z] = hashlib.sha256(memoryview(bufs[k].numpy()).cast("B")).hexdigest()
+
+    with cf.ThreadPoolExecutor(batch) as pool:
+        for z0 in range(0, n_z, batch):
+            zs = list(range(z0, min(n_z, z0 + batch)))
+            for k, z in enumerate(zs):
+                bufs[k].copy_(flat[z * per:(z + 1) * per])
+            list(pool.map(lambda kz: digest(*kz), enumerate(zs)))
     return out
 
 

@@ -90,11 +90,15 @@ def test_inverse_refused_for_even_dims():
         hprime_device(to_device(H), inverse=True)
 
 
-@pytest.mark.parametrize("cfg", ["C1", "C2", "C4", "C3"])
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4", "C3",
+                                 pytest.param("C5", marks=pytest.mark.slow)])
 def test_baseline_config_matches_reference_digests(cfg):
     """Full-size BASELINE configs: every plane of the device H' has the SHA-256
-    of the reference's H' (computed by lfbp itself, tests/golden/)."""
+    of the reference's H' (computed by lfbp itself, tests/golden/).  C5
+    (71 GB in + 71 GB out on one GPU) runs with LFBP_TEST_C5=1."""
     torch = _torch()
+    if cfg == "C5" and not os.environ.get("LFBP_TEST_C5"):
+        pytest.skip("C5 full size is opt-in (LFBP_TEST_C5=1)")
     from paper_2003_09133_b200 import f_order_empty, hprime_device
     from paper_2003_09133_b200.configs import WORKLOADS
     from paper_2003_09133_b200.synth import baseline_psf
@@ -106,12 +110,13 @@ def test_baseline_config_matches_reference_digests(cfg):
     tdt = torch.float32 if w.itemsize == 4 else torch.float64
     src = f_order_empty(w.shape, tdt)
     # generate plane slabs on the host and upload (the generator is pinned by digests)
-    step = max(1, (512 << 20) // (w.plane_elems * w.itemsize))
+    step = max(8, (512 << 20) // (w.plane_elems * w.itemsize))
     flat = src.permute(4, 3, 2, 1, 0).reshape(-1)
     for z0 in range(0, w.shape[4], step):
         z1 = min(w.shape[4], z0 + step)
         slab = baseline_psf(w, z0, z1)
         flat[z0 * w.plane_elems:z1 * w.plane_elems].copy_(torch.from_numpy(slab.reshape(-1, order="F")))
+        del slab
     in_dig = plane_digests(src, w.shape)
     assert in_dig == d["input_plane_sha256"]
     out = hprime_device(src)
@@ -147,6 +152,8 @@ def test_random_shapes_match_oracle(shape, dtype):
     {"LFBP_STAGES": "1"}, {"LFBP_STAGES": "2", "LFBP_CONSUMER_WARPS": "1"},
     {"LFBP_STAGE_KB": "1"}, {"LFBP_STAGE_KB": "200", "LFBP_STAGE_MAX_KB": "200"},
     {"LFBP_CTAS_PER_SM": "1", "LFBP_CONSUMER_WARPS": "16"}, {"LFBP_BAND": "3"},
+    {"LFBP_SUBWARP": "8"}, {"LFBP_SUBWARP": "32"}, {"LFBP_SUBWARP": "16", "LFBP_CONSUMER_WARPS": "3"},
+    {"LFBP_SUBWARP": "8", "LFBP_STAGE_MAX_KB": "2", "LFBP_STAGES": "2"},
 ])
 @pytest.mark.parametrize("shape,dtype", [((55, 55, 11, 11, 2), np.float32), ((27, 20, 13, 5, 2), np.float64),
                                          ((66, 41, 21, 9, 1), np.float32)])
