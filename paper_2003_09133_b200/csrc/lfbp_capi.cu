@@ -149,6 +149,8 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   if (d[2] * (row_full + 32) <= stage_max) {
     int64_t J = stage_target / (d[2] * row_full);
     J = std::max<int64_t>(1, std::min<int64_t>(J, d[1]));
+    // small problems: keep >= 8 units per SM so the smem ring actually pipelines
+    while (J > 1 && z_count * ((d[1] + J - 1) / J) * d[3] < int64_t(8) * dp.sm_count) J = (J + 1) / 2;
     const int jcap = env_int("LFBP_BAND", 0);
     if (jcap > 0) J = std::min<int64_t>(J, jcap);
     p.J = static_cast<int32_t>(J);
