@@ -82,7 +82,8 @@ __device__ __forceinline__ void st_v2_64_na(void* p, unsigned long long a, unsig
 // consumer warps read it with a few LDS instead of re-decoding.
 struct UnitHdr {
   long long plane_off;  // z * plane_elems
-  int32_t y, t0, jb, i_lo, i_hi, s_lo, o0, pad;
+  int32_t y, t0, jb, i_lo, i_hi, s_lo, o0;
+  int32_t next_row;     // work counter: consumer warps claim rows with atomicAdd
 };
 constexpr int kHdrBytes = 64;
 
@@ -185,6 +186,7 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
     h->i_hi = w.i_hi;
     h->s_lo = w.s_lo;
     h->o0 = static_cast<int32_t>(b0 & 15);
+    h->next_row = 0;
   }
   tx = __reduce_add_sync(0xffffffffu, tx);
   __syncwarp();                                    // header and tail stores before the release
@@ -262,14 +264,20 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
   const uint32_t inc_x = static_cast<uint32_t>(p.gx_inc);              // (W*VE) mod n_x
   const int32_t inc_a = p.gx_inc * rp - W * VE * E;                    // smem step of W groups
   const bool wrap1 = n_x >= VE;
-  const int32_t rstep = nc * R;
   T* dz = reinterpret_cast<T*>(dst) + h.plane_off;
-  int32_t tl = 0, xp = cw * R + lane / W;
-  while (xp >= n_x) {
-    xp -= n_x;
-    ++tl;
-  }
-  while (tl < h.jb) {
+  int* next_row = &reinterpret_cast<UnitHdr*>(const_cast<uint8_t*>(stage))->next_row;
+  const int32_t rows = h.jb * n_x;
+  for (;;) {
+    // claim the next R rows of the unit (dynamic balance across warps)
+    int32_t r0 = 0;
+    if (lane == 0) r0 = atomicAdd(next_row, R);
+    r0 = __shfl_sync(0xffffffffu, r0, 0);
+    if (r0 >= rows) break;
+    const int32_t r = r0 + lane / W;
+    do {  // this sub-warp's row (none past the end of the unit)
+    if (r >= rows) break;
+    const int32_t tl = static_cast<int32_t>(hp_div(p.nx_div, static_cast<uint32_t>(r)));
+    const int32_t xp = r - tl * n_x;
     const int32_t t = h.t0 + tl;
     const bool zero_row = t >= p.v_t;  // dropped source row t = n_t - 1 (even n_t)
     const int32_t j = zero_row ? static_cast<int32_t>(p.n_t) - 1 : 2 * p.c_t - t;
@@ -318,11 +326,7 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
         }
       }
     }
-    xp += rstep;
-    while (xp >= n_x) {
-      xp -= n_x;
-      ++tl;
-    }
+    } while (0);
   }
 }
 

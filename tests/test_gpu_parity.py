@@ -188,6 +188,31 @@ def test_z_range_writes_only_its_planes():
     assert (got[..., :2] == -7.0).all() and (got[..., 5:] == -7.0).all()
 
 
+@pytest.mark.parametrize("cfg", ["C2", "C4"])
+def test_full_size_involution_on_device(cfg):
+    """rearrange(rearrange(H)) == H byte for byte at full BASELINE size
+    (odd n_s, n_t: the map is an involution), compared on the device."""
+    torch = _torch()
+    from paper_2003_09133_b200 import f_order_empty
+    from paper_2003_09133_b200.configs import WORKLOADS
+    from paper_2003_09133_b200.verify import involution_check
+    w = WORKLOADS[cfg]
+    src = f_order_empty(w.shape, torch.float32 if w.itemsize == 4 else torch.float64)
+    src.permute(4, 3, 2, 1, 0).reshape(-1).view(torch.int32 if w.itemsize == 4 else torch.int64).random_()
+    assert involution_check(src) == (0, -1)
+
+
+def test_empty_z_range_is_a_no_op():
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device
+    H = np.ones((5, 5, 3, 3, 2), order="F", dtype=np.float32)
+    src = to_device(H)
+    out = torch.full_like(src, 3.0)
+    hprime_device(src, out=out, z_range=(1, 1))
+    torch.cuda.synchronize()
+    assert (out == 3.0).all()
+
+
 def test_unaligned_total_size_tail_loads():
     """Arrays whose byte size is not a multiple of 16 (tail words loaded
     without bulk copies), in an exact-size allocation."""

@@ -119,3 +119,30 @@ def test_argument_errors():
         == _native.ERR_EVEN_PIXEL_DIMS
     assert lib.lfbp_hprime_host(None, None, _native.dims_array((5, 5, 2, 3, 1)), 1, 0, 0, 0) \
         == _native.ERR_INVALID_DIMS
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No CPU fallback: without libhprime.so every compute call raises."""
+    from paper_2003_09133_b200 import Dims5, NativeError, PsfArray, compute_backprojection
+    monkeypatch.setattr(_native, "_lib", None)
+    monkeypatch.setattr(_native, "LIB_PATH", str(tmp_path / "missing.so"))
+    with pytest.raises(NativeError):
+        compute_backprojection(PsfArray(Dims5(3, 3, 3, 3, 1), np.ones((3, 3, 3, 3, 1))))
+
+
+def test_dropin_mirrors_reference_errors_and_types():
+    from paper_2003_09133_b200 import BackprojArray, Dims5, EvenPixelDims, InvalidDims, PsfArray
+    from paper_2003_09133_b200 import compute_psf_from_backprojection
+    with pytest.raises(InvalidDims):
+        Dims5(True, 3, 3, 3, 1)
+    with pytest.raises(InvalidDims):
+        PsfArray(Dims5(3, 3, 3, 3, 1), -np.ones((3, 3, 3, 3, 1)))
+    with pytest.raises(InvalidDims):
+        PsfArray(Dims5(3, 3, 3, 3, 1), np.full((3, 3, 3, 3, 1), np.nan))
+    psf = PsfArray(Dims5(3, 3, 3, 3, 1), np.ones((3, 3, 3, 3, 1), dtype=np.int32))
+    assert psf.dtype == np.float64 and not psf.data.flags.writeable and psf.data.flags.f_contiguous
+    with pytest.raises(AttributeError):
+        psf.dims = None
+    # the even-dims inverse is refused before any device work
+    with pytest.raises(EvenPixelDims):
+        compute_psf_from_backprojection(BackprojArray._wrap(Dims5(4, 5, 3, 3, 1), np.ones((4, 5, 3, 3, 1), order="F")))
