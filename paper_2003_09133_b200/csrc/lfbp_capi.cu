@@ -94,7 +94,7 @@ int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 // Tunable launch knobs.  Environment variables (LFBP_STAGES, LFBP_STAGE_KB,
 // LFBP_CONSUMER_WARPS, LFBP_SUBWARP) override them for sweeps and tests.
 struct Knobs {
-  int stages = 3;      // smem ring depth
+  int stages = 4;      // smem ring depth
   int stage_kb = 48;   // target bytes of one staged unit (sets the t-band J)
   int cwarps = 12;     // consumer warps per CTA
   int subwarp = 0;     // lanes per output row; 0 = by row length
@@ -114,8 +114,8 @@ bool env_knobs_set() {
 // Candidates tried by the autotuner (measured best plans of C1..C5 and
 // neighbours; every one is bit-exact, they differ only in speed).
 const Knobs kCandidates[] = {
-    {3, 48, 12, 8}, {4, 48, 12, 16}, {3, 16, 4, 16}, {3, 32, 8, 16},
-    {2, 16, 8, 8},  {3, 16, 6, 32},  {2, 32, 4, 8},  {4, 32, 8, 16},
+    {4, 48, 16, 16}, {3, 48, 12, 8}, {4, 32, 16, 32}, {4, 48, 8, 8},
+    {4, 32, 12, 32}, {4, 32, 8, 32}, {2, 48, 4, 8},  {4, 32, 8, 16},
 };
 
 // Work-unit shape, smem ring and persistent grid for one launch.
@@ -208,7 +208,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   // lanes per output row: enough 16-byte groups per lane to amortise the row setup
   const int64_t groups = (std::min<int64_t>(p.C, d[0]) * E + 15) / 16 + 1;
   int W = env_int("LFBP_SUBWARP", kn.subwarp);
-  if (W != 8 && W != 16 && W != 32) W = groups <= 64 ? 8 : groups <= 128 ? 16 : 32;
+  if (W != 8 && W != 16 && W != 32) W = groups <= 32 ? 8 : groups <= 64 ? 16 : 32;
   p.sub_width = W;
   p.gx_inc = static_cast<int32_t>((W * (16 / E)) % d[2]);
   p.nx_div = hp_fastdiv_make(static_cast<uint32_t>(d[2]));
