@@ -46,6 +46,9 @@ extern "C" {
 
 /* flags for lfbp_hprime_host / lfbp_hprime_multi */
 #define LFBP_HOST_REGISTER 1   /* pin pageable host buffers for the call (cudaHostRegister) */
+#define LFBP_HOST_STAGE 2      /* copy pageable host buffers through pinned staging chunks
+                                  (multi-threaded memcpy overlapped with the DMA); wins over
+                                  LFBP_HOST_REGISTER when both are set */
 
 /* Validate (n_s, n_t, n_x, n_y, n_z) like Dims5 (arrays.py:53-67).
  * Returns LFBP_OK or LFBP_ERR_INVALID_DIMS. No GPU needed. */
@@ -65,8 +68,9 @@ int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dt
 
 /* Host-to-host H' on one GPU: the z-planes are streamed through the device in
  * chunks (H2D, kernel and D2H overlapped on three streams).  `src` and `dst`
- * are host arrays of the whole shape; pinned memory gives full PCIe speed,
- * pageable memory is pinned for the call when flags has LFBP_HOST_REGISTER.
+ * are host arrays of the whole shape; pinned memory gives full PCIe speed;
+ * pageable memory is staged through pinned chunks (LFBP_HOST_STAGE) or
+ * pinned for the call (LFBP_HOST_REGISTER), else the driver stages it.
  * Synchronous: returns when dst is complete. */
 int lfbp_hprime_host(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse,
                      int device, int flags);

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhprime.s
 OK, ERR_INVALID_DIMS, ERR_EVEN_PIXEL_DIMS, ERR_CUDA, ERR_ARGUMENT, ERR_UNSUPPORTED = range(6)
 F32, F64 = 1, 2
 HOST_REGISTER = 1
+HOST_STAGE = 2
 
 EXPORTS = (
     "lfbp_check_dims", "lfbp_dropped_source_count", "lfbp_hprime_device", "lfbp_hprime_host",

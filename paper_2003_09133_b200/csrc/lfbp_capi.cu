@@ -12,7 +12,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -183,7 +185,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   int cwarps = env_int("LFBP_CONSUMER_WARPS", kn.cwarps);
   if (cwarps <= 0) cwarps = 12;
   cwarps = std::max(1, std::min(16, cwarps));
-  const int threads = 32 * (1 + cwarps);
+  const int threads = 32 * (1 + cwarps);  // producer + consumers
   p.threads = threads;
 
   const int64_t units = z_count * p.n_chunks * int64_t(p.n_bands) * d[3];
@@ -316,6 +318,74 @@ int check_common(const int64_t dims[5], int dtype, int inverse) {
 
 int64_t plane_elems(const int64_t d[5]) { return d[0] * d[1] * d[2] * d[3]; }
 
+// ---- host memcpy thread pool (pageable <-> pinned staging) ----
+class CopyPool {
+ public:
+  explicit CopyPool(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { run(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  // memcpy(dst, src, n) split over all workers; returns when done
+  void copy(void* dst, const void* src, size_t n) {
+    if (n < (size_t(4) << 20) || th_.empty()) {
+      memcpy(dst, src, n);
+      return;
+    }
+    std::lock_guard<std::mutex> one_job(call_mu_);  // callers from several device threads take turns
+    std::unique_lock<std::mutex> lk(mu_);
+    dst_ = static_cast<uint8_t*>(dst);
+    src_ = static_cast<const uint8_t*>(src);
+    n_ = n;
+    pending_ = int(th_.size());
+    ++gen_;
+    cv_.notify_all();
+    done_.wait(lk, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void run(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      const size_t parts = th_.size();
+      const size_t chunk = (n_ / parts + 63) & ~size_t(63);
+      const size_t a = std::min(n_, chunk * i), b = std::min(n_, a + chunk);
+      uint8_t* d = dst_;
+      const uint8_t* s = src_;
+      lk.unlock();
+      if (b > a) memcpy(d + a, s + a, b - a);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex call_mu_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  uint8_t* dst_ = nullptr;
+  const uint8_t* src_ = nullptr;
+  size_t n_ = 0;
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+CopyPool& copy_pool() {
+  static CopyPool pool(std::max(1, std::min(16, env_int("LFBP_COPY_THREADS",
+                                                        int(std::thread::hardware_concurrency()) / 2))));
+  return pool;
+}
+
 // ---- host pipeline workspace (one per device, reused across calls) ----
 constexpr int kPipe = 3;
 
@@ -328,6 +398,9 @@ struct Workspace {
   cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
   cudaEvent_t h2d_done[kPipe] = {}, cmp_done[kPipe] = {}, d2h_done[kPipe] = {};
   bool init = false;
+  size_t stage_cap = 0;             // pinned staging for pageable host arrays
+  void* pin_in[kPipe] = {};
+  void* pin_out[kPipe] = {};
 };
 
 std::mutex g_ws_mu;
@@ -370,6 +443,31 @@ int ws_reserve(Workspace& w, size_t bytes) {
   return LFBP_OK;
 }
 
+int ws_reserve_staging(Workspace& w, size_t bytes) {
+  if (bytes <= w.stage_cap) return LFBP_OK;
+  for (int k = 0; k < kPipe; ++k) {
+    if (w.pin_in[k]) cudaFreeHost(w.pin_in[k]);
+    if (w.pin_out[k]) cudaFreeHost(w.pin_out[k]);
+    w.pin_in[k] = w.pin_out[k] = nullptr;
+  }
+  w.stage_cap = 0;
+  for (int k = 0; k < kPipe; ++k) {
+    HP_CUDA(cudaHostAlloc(&w.pin_in[k], bytes, cudaHostAllocPortable));
+    HP_CUDA(cudaHostAlloc(&w.pin_out[k], bytes, cudaHostAllocPortable));
+  }
+  w.stage_cap = bytes;
+  return LFBP_OK;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 struct HostPin {
   void* ptr = nullptr;
   bool registered = false;
@@ -406,21 +504,51 @@ int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, in
   const int64_t target = int64_t(env_int("LFBP_CHUNK_MB", 64)) << 20;
   const int64_t cp = std::max<int64_t>(1, std::min<int64_t>(nz, target / std::max<int64_t>(pb, 1)));
   const int64_t n_chunks = (nz + cp - 1) / cp;
+  // pageable arrays: stage through pinned buffers (parallel host memcpy
+  // overlapped with the DMA), or pin them in place, or let the driver stage
+  const bool stage_in = (flags & LFBP_HOST_STAGE) && !is_pinned(src + z0 * pb);
+  const bool stage_out = (flags & LFBP_HOST_STAGE) && !is_pinned(dst + z0 * pb);
+  const int reg_flags = flags & LFBP_HOST_REGISTER;
   HostPin pin_in, pin_out;
-  int rc = maybe_pin(pin_in, src + z0 * pb, size_t(nz * pb), flags);
+  int rc = stage_in ? LFBP_OK : maybe_pin(pin_in, src + z0 * pb, size_t(nz * pb), reg_flags);
   if (rc) return rc;
-  rc = maybe_pin(pin_out, dst + z0 * pb, size_t(nz * pb), flags);
+  rc = stage_out ? LFBP_OK : maybe_pin(pin_out, dst + z0 * pb, size_t(nz * pb), reg_flags);
   if (rc) return rc;
   Workspace& w = workspace(dev);
   std::lock_guard<std::mutex> lk(w.mu);
   rc = ws_reserve(w, size_t(cp * pb));
   if (rc) return rc;
+  if (stage_in || stage_out) {
+    rc = ws_reserve_staging(w, size_t(cp * pb));
+    if (rc) return rc;
+  }
+  auto chunk_range = [&](int64_t c, int64_t& a, size_t& bytes) {
+    a = z0 + c * cp;
+    bytes = size_t(std::min<int64_t>(cp, z1 - a) * pb);
+  };
+  auto drain = [&](int64_t c) -> int {  // staged output of chunk c -> dst
+    int64_t a;
+    size_t bytes;
+    chunk_range(c, a, bytes);
+    const int k = int(c % kPipe);
+    HP_CUDA(cudaEventSynchronize(w.d2h_done[k]));
+    copy_pool().copy(dst + a * pb, w.pin_out[k], bytes);
+    return LFBP_OK;
+  };
   for (int64_t c = 0; c < n_chunks; ++c) {
     const int k = int(c % kPipe);
-    const int64_t a = z0 + c * cp, planes = std::min<int64_t>(cp, z1 - a);
-    const size_t bytes = size_t(planes * pb);
+    int64_t a;
+    size_t bytes;
+    chunk_range(c, a, bytes);
+    const int64_t planes = int64_t(bytes) / pb;
+    const uint8_t* h_src = src + a * pb;
+    if (stage_in) {
+      if (c >= kPipe) HP_CUDA(cudaEventSynchronize(w.h2d_done[k]));  // pin_in[k] free
+      copy_pool().copy(w.pin_in[k], h_src, bytes);
+      h_src = static_cast<const uint8_t*>(w.pin_in[k]);
+    }
     if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_h2d, w.cmp_done[k], 0));  // in[k] consumed
-    HP_CUDA(cudaMemcpyAsync(w.in[k], src + a * pb, bytes, cudaMemcpyHostToDevice, w.s_h2d));
+    HP_CUDA(cudaMemcpyAsync(w.in[k], h_src, bytes, cudaMemcpyHostToDevice, w.s_h2d));
     HP_CUDA(cudaEventRecord(w.h2d_done[k], w.s_h2d));
     HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.h2d_done[k], 0));
     if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.d2h_done[k], 0));  // out[k] drained
@@ -434,9 +562,20 @@ int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, in
     if (rc) return rc;
     HP_CUDA(cudaEventRecord(w.cmp_done[k], w.s_cmp));
     HP_CUDA(cudaStreamWaitEvent(w.s_d2h, w.cmp_done[k], 0));
-    HP_CUDA(cudaMemcpyAsync(dst + a * pb, w.out[k], bytes, cudaMemcpyDeviceToHost, w.s_d2h));
+    HP_CUDA(cudaMemcpyAsync(stage_out ? static_cast<uint8_t*>(w.pin_out[k]) : dst + a * pb, w.out[k], bytes,
+                            cudaMemcpyDeviceToHost, w.s_d2h));
     HP_CUDA(cudaEventRecord(w.d2h_done[k], w.s_d2h));
+    // chunk c - (kPipe - 1) frees its pinned output before pin_out is reused
+    if (stage_out && c >= kPipe - 1) {
+      rc = drain(c - (kPipe - 1));
+      if (rc) return rc;
+    }
   }
+  if (stage_out)
+    for (int64_t c = std::max<int64_t>(0, n_chunks - (kPipe - 1)); c < n_chunks; ++c) {
+      rc = drain(c);
+      if (rc) return rc;
+    }
   HP_CUDA(cudaStreamSynchronize(w.s_d2h));
   HP_CUDA(cudaStreamSynchronize(w.s_cmp));
   HP_CUDA(cudaStreamSynchronize(w.s_h2d));

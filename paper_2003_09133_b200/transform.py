@@ -67,7 +67,11 @@ def dropped_source_count(dims) -> int:
 
 
 def _host_flags() -> int:
-    return 0 if os.environ.get("LFBP_NO_HOST_REGISTER") else _native.HOST_REGISTER
+    """How pageable host arrays reach the GPU (LFBP_HOST_MODE): "stage"
+    (default: pinned staging chunks filled by a memcpy thread pool, overlapped
+    with the DMA), "register" (pin in place for the call) or "driver"."""
+    mode = os.environ.get("LFBP_HOST_MODE", "stage")
+    return {"stage": _native.HOST_STAGE, "register": _native.HOST_REGISTER, "driver": 0}.get(mode, _native.HOST_STAGE)
 
 
 def _pinned_empty(shape, dtype) -> np.ndarray:

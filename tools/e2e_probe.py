@@ -96,18 +96,15 @@ def main():
     pageable = np.array(H, order="F")
     pageable.flags.writeable = False
     psf = PsfArray._wrap(Dims5(*w.shape), pageable)
-    for reg in (True, False):
-        if reg:
-            os.environ.pop("LFBP_NO_HOST_REGISTER", None)
-        else:
-            os.environ["LFBP_NO_HOST_REGISTER"] = "1"
+    for reg in ("stage", "register", "driver"):
+        os.environ["LFBP_HOST_MODE"] = reg
         out = {}
 
         def dropin():
             out["bp"] = compute_backprojection(psf)
         best, med = timed(dropin)
         dig = hashlib.sha256(out["bp"].data.tobytes(order="F")).hexdigest()
-        print(json.dumps({"path": "drop-in pageable input", "host_register": reg, "best_ms": round(best * 1e3, 2),
+        print(json.dumps({"path": "drop-in pageable input", "host_mode": reg, "best_ms": round(best * 1e3, 2),
                           "med_ms": round(med * 1e3, 2), "GBps_rw": round(step_bytes / best / 1e9, 2),
                           "same": dig == ref}), flush=True)
 

@@ -1,7 +1,7 @@
 #!/bin/bash
 # tests, default bench (C2), per-config kernel benches, ncu of the tuned C2 kernel
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+timeout 420 python -m pytest tests -x -q -m gpu --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 timeout 300 python bench.py > gpurun_out/bench.log 2>&1; echo bench_rc=$?
 for c in C1 C3 C4 C5; do
   timeout 600 python bench.py --config $c --steps 20 --no-cpu --no-e2e > gpurun_out/bench_$c.log 2>&1; echo bench_${c}_rc=$?

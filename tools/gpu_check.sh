@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 set -x
 nproc; free -g | head -2
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+timeout 420 python -m pytest tests -x -q -m gpu --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 timeout 300 python bench.py > gpurun_out/bench.log 2>&1; echo bench_rc=$?
 timeout 300 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref_rc=$?
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e --no-verify"
