@@ -257,3 +257,41 @@ def test_multi_device_host_launcher_single_gpu():
     out2 = np.empty_like(H, order="F")
     rearrange_multi_host(H, out2, [0, 0])
     assert fbytes(out2) == fbytes(out)
+
+
+@pytest.mark.parametrize("mode", ["stage", "register", "driver"])
+def test_dropin_pageable_host_modes_multi_chunk(monkeypatch, mode):
+    """Pageable numpy input through every host mode, with chunks small enough
+    that the pipeline (and the staging thread pool) runs many chunks."""
+    _torch()
+    from paper_2003_09133_b200 import Dims5, PsfArray, compute_backprojection
+    from paper_2003_09133_b200.configs import WORKLOADS
+    from paper_2003_09133_b200.synth import baseline_psf
+    monkeypatch.setenv("LFBP_HOST_MODE", mode)
+    monkeypatch.setenv("LFBP_CHUNK_MB", "8")
+    w = WORKLOADS["C2"].with_planes(7)             # 240 MB, 7 chunks of one 34 MB plane
+    H = baseline_psf(w)
+    bp = compute_backprojection(PsfArray._wrap(Dims5(*w.shape), H))
+    assert fbytes(bp.data) == fbytes(hprime_oracle(H, threads=7))
+
+
+def test_multi_host_staged_pageable_output():
+    """lfbp_hprime_multi with pageable src and dst (staging both ways)."""
+    _torch()
+    import ctypes
+
+    from paper_2003_09133_b200 import _native
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    shape = (101, 99, 9, 7, 12)
+    H = random_psf_like_reference(shape, density=1.0, seed=4, dtype=np.float32)
+    out = np.empty_like(H, order="F")
+    devs = (ctypes.c_int * 2)(0, 0)
+    import os
+    os.environ["LFBP_CHUNK_MB"] = "1"
+    try:
+        rc = _native.lib().lfbp_hprime_multi(H.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p),
+                                             _native.dims_array(shape), _native.F32, 0, 2, devs, _native.HOST_STAGE)
+    finally:
+        del os.environ["LFBP_CHUNK_MB"]
+    _native.check(rc)
+    assert fbytes(out) == fbytes(hprime_oracle(H))
