@@ -231,6 +231,64 @@ __device__ __forceinline__ void load_group_general(typename Word<E>::T* v, uint3
   }
 }
 
+// The VE values of one 16-byte output group whose first element has source
+// phase x0 and smem address a0.  WRAP1 (n_x >= VE): x wraps at most once
+// inside the group, so each load picks one of two bases.
+template <int E, bool WRAP1>
+__device__ __forceinline__ void load_group(typename Word<E>::T* v, uint32_t a0, uint32_t x0, int32_t n_x,
+                                           int32_t step, int32_t nr) {
+  constexpr int VE = 16 / E;
+  if constexpr (WRAP1) {
+    const int32_t d = n_x - static_cast<int32_t>(x0);   // elements before the wrap
+    const uint32_t aw = a0 - nr;
+    v[0] = lds<E>(a0);
+#pragma unroll
+    for (int q = 1; q < VE; ++q) v[q] = lds<E>((q >= d ? aw : a0) + q * step);
+  } else {
+    load_group_general<E>(v, a0, x0, n_x, step, nr);
+  }
+}
+
+// One sub-warp lane's groups g, g+W, ... of a row: a masked leading group
+// (only when the row starts inside a 16-byte group), unmasked full groups,
+// a masked trailing group.
+template <int E, bool WRAP1>
+__device__ __forceinline__ void row_groups(typename Word<E>::T* o, int32_t g, int32_t ng, bool last_full, int32_t i0,
+                                           int32_t i_lo, int32_t i_end, uint32_t x0, uint32_t a0, int32_t n_x,
+                                           int32_t step, int32_t nr, int32_t W, uint32_t inc_x, int32_t inc_a) {
+  using T = typename Word<E>::T;
+  constexpr int VE = 16 / E;
+  const int32_t inc_a_w = inc_a - nr;
+  auto advance = [&]() {
+    o += W * VE;
+    i0 += W * VE;
+    x0 += inc_x;
+    const bool wr = x0 >= static_cast<uint32_t>(n_x);
+    x0 = wr ? x0 - n_x : x0;
+    a0 += wr ? inc_a_w : inc_a;
+  };
+  auto masked = [&]() {
+    T v[VE];
+    load_group<E, WRAP1>(v, a0, x0, n_x, step, nr);
+#pragma unroll
+    for (int q = 0; q < VE; ++q)
+      if (i0 + q >= i_lo && i0 + q < i_end) o[q] = v[q];
+  };
+  if (i0 < i_lo) {  // leading partial group (g == 0)
+    masked();
+    advance();
+    g += W;
+  }
+  const int32_t g_hi = last_full ? ng : ng - 1;
+  for (; g < g_hi; g += W) {
+    T v[VE];
+    load_group<E, WRAP1>(v, a0, x0, n_x, step, nr);
+    st_vec<E>(o, v);
+    advance();
+  }
+  if (g < ng) masked();  // trailing partial group
+}
+
 // Consumer warps (cw of nc) write the J * n_x output rows of the unit staged
 // at `stage` (smem address `stage_s`).  Each warp is split into 32/W
 // sub-warps of W lanes (W = p.sub_width); a sub-warp owns one output row at a
@@ -263,7 +321,6 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
   const int32_t zmis = static_cast<int32_t>(h.plane_off & (VE - 1));
   const uint32_t inc_x = static_cast<uint32_t>(p.gx_inc);              // (W*VE) mod n_x
   const int32_t inc_a = p.gx_inc * rp - W * VE * E;                    // smem step of W groups
-  const bool wrap1 = n_x >= VE;
   T* dz = reinterpret_cast<T*>(dst) + h.plane_off;
   int* next_row = &reinterpret_cast<UnitHdr*>(const_cast<uint8_t*>(stage))->next_row;
   const int32_t rows = h.jb * n_x;
@@ -293,37 +350,15 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
       int32_t g = sl;
       if (g < ng) {
         // smem address of (x, i) = base + x*rp + (tl*n_s - s_lo + 2c_s - i)*E
-        uint32_t x0 = hp_mod(p.nx_div, static_cast<uint32_t>(xp + gs + p.nx_off + VE * n_x + g * VE));
-        uint32_t a0 = base + static_cast<uint32_t>((tl * n_s - h.s_lo + 2 * p.c_s - gs - g * VE) * E) + x0 * rp;
-        int32_t i0 = gs + g * VE;
-        T* o = orow + i0;
-        for (; g < ng; g += W) {
-          T v[VE];
-          if (wrap1) {  // at most one wrap inside a group
-            const int32_t d = n_x - static_cast<int32_t>(x0);
-            const uint32_t aw = a0 - nr;
-            v[0] = lds<E>(a0);
-#pragma unroll
-            for (int q = 1; q < VE; ++q) v[q] = lds<E>((q >= d ? aw : a0) + q * step);
-          } else {
-            load_group_general<E>(v, a0, x0, n_x, step, nr);
-          }
-          if (i0 >= i_lo && i0 + VE <= i_end) {
-            st_vec<E>(o, v);
-          } else {
-#pragma unroll
-            for (int q = 0; q < VE; ++q)
-              if (i0 + q >= i_lo && i0 + q < i_end) o[q] = v[q];
-          }
-          o += W * VE;
-          i0 += W * VE;
-          x0 += inc_x;
-          a0 += inc_a;
-          if (x0 >= static_cast<uint32_t>(n_x)) {
-            x0 -= n_x;
-            a0 -= nr;
-          }
-        }
+        const uint32_t x0 = hp_mod(p.nx_div, static_cast<uint32_t>(xp + gs + p.nx_off + VE * n_x + g * VE));
+        const uint32_t a0 =
+            base + static_cast<uint32_t>((tl * n_s - h.s_lo + 2 * p.c_s - gs - g * VE) * E) + x0 * rp;
+        const int32_t i0 = gs + g * VE;
+        const bool last_full = ((i_end - gs) & (VE - 1)) == 0;
+        if (n_x >= VE)
+          row_groups<E, true>(orow + i0, g, ng, last_full, i0, i_lo, i_end, x0, a0, n_x, step, nr, W, inc_x, inc_a);
+        else
+          row_groups<E, false>(orow + i0, g, ng, last_full, i0, i_lo, i_end, x0, a0, n_x, step, nr, W, inc_x, inc_a);
       }
     }
     } while (0);

@@ -116,8 +116,8 @@ bool env_knobs_set() {
 // Candidates tried by the autotuner (measured best plans of C1..C5 and
 // neighbours; every one is bit-exact, they differ only in speed).
 const Knobs kCandidates[] = {
-    {4, 48, 16, 16}, {3, 48, 12, 8}, {4, 32, 16, 32}, {4, 48, 8, 8},
-    {4, 32, 12, 32}, {4, 32, 8, 32}, {2, 48, 4, 8},  {4, 32, 8, 16},
+    {3, 48, 8, 8},   {3, 48, 16, 16}, {4, 48, 8, 16}, {4, 32, 16, 32},
+    {4, 48, 16, 32}, {3, 48, 8, 32},  {2, 48, 4, 8},  {4, 32, 8, 16},
 };
 
 // Work-unit shape, smem ring and persistent grid for one launch.
@@ -268,27 +268,40 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
   cudaEvent_t e0, e1;
   HP_CUDA(cudaEventCreate(&e0));
   HP_CUDA(cudaEventCreate(&e1));
-  float best_ms = 1e30f;
-  bool found = false;
-  for (const Knobs& c : kCandidates) {
-    HpPlan p;
-    if (make_plan(p, dims, E, z_begin, z_count, total, key.dev, c) != LFBP_OK) continue;
-    int rc = launch(p, src, dst, st);
-    if (rc) return rc;
-    float ms = 1e30f;
-    for (int r = 0; r < 2; ++r) {
+  // candidates interleaved over rounds (decorrelates clock / power drift);
+  // score = median of the per-round launch times
+  constexpr int kCand = int(sizeof(kCandidates) / sizeof(kCandidates[0]));
+  constexpr int kRounds = 3;
+  HpPlan plans[kCand];
+  bool ok[kCand];
+  float t[kCand][kRounds];
+  for (int c = 0; c < kCand; ++c) {
+    ok[c] = make_plan(plans[c], dims, E, z_begin, z_count, total, key.dev, kCandidates[c]) == LFBP_OK;
+    if (ok[c]) {
+      int rc = launch(plans[c], src, dst, st);  // warm
+      if (rc) return rc;
+    }
+  }
+  for (int r = 0; r < kRounds; ++r)
+    for (int c = 0; c < kCand; ++c) {
+      if (!ok[c]) continue;
       HP_CUDA(cudaEventRecord(e0, st));
-      rc = launch(p, src, dst, st);
+      int rc = launch(plans[c], src, dst, st);
       if (rc) return rc;
       HP_CUDA(cudaEventRecord(e1, st));
       HP_CUDA(cudaEventSynchronize(e1));
-      float t = 0.f;
-      HP_CUDA(cudaEventElapsedTime(&t, e0, e1));
-      ms = std::min(ms, t);
+      HP_CUDA(cudaEventElapsedTime(&t[c][r], e0, e1));
     }
-    if (ms < best_ms) {
-      best_ms = ms;
-      best = c;
+  float best_ms = 1e30f;
+  bool found = false;
+  for (int c = 0; c < kCand; ++c) {
+    if (!ok[c]) continue;
+    float v[kRounds];
+    for (int r = 0; r < kRounds; ++r) v[r] = t[c][r];
+    std::sort(v, v + kRounds);
+    if (v[kRounds / 2] < best_ms) {
+      best_ms = v[kRounds / 2];
+      best = kCandidates[c];
       found = true;
     }
   }
