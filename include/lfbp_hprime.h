@@ -21,6 +21,8 @@
  *   lfbp_dropped_source_count -> dropped_source_count transform.py:106-110
  *   lfbp_compare_device    -> the bitwise np.array_equal verification of
  *                             bench.py:88 / cli.py:145-150, on the device
+ *   lfbp_plane_sums_device -> sum_forward_plane / sum_backward_plane
+ *                             arrays.py:211-239 (acceptance criterion 3)
  * Error codes mirror the reference's exceptions (errors.py:12-13, 32-33).
  */
 #ifndef LFBP_HPRIME_H
@@ -90,6 +92,15 @@ int lfbp_shard_planes(int64_t n_z, int n_shards, int shard, int64_t* z_begin, in
  * equal).  Synchronous. */
 int lfbp_compare_device(const void* a, const void* b, int64_t nbytes, int64_t* n_diff,
                         int64_t* first_diff, void* stream);
+
+/* Sorted-order float64 sums of every (s, t) pattern slice of depth planes
+ * [z_begin, z_end) of a device array (K3): out[(z - z_begin)*n_s*n_t + t*n_s + s]
+ * equals, bit for bit, the reference's sum_forward_plane / sum_backward_plane
+ * (arrays.py:211-239: np.sort then numpy's pairwise float64 sum).  `out` is a
+ * device buffer of n_s*n_t*(z_end - z_begin) doubles.  Asynchronous on
+ * `stream`.  n_x*n_y must be <= 8192. */
+int lfbp_plane_sums_device(const void* src, double* out, const int64_t dims[5], int dtype, int64_t z_begin,
+                           int64_t z_end, void* stream);
 
 /* The launch plan the kernel would use, as a JSON object in `buf` (for
  * tests, tuning and DESIGN.md).  Uses the current device's properties, or

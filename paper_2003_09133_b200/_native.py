@@ -22,7 +22,7 @@ HOST_STAGE = 2
 EXPORTS = (
     "lfbp_check_dims", "lfbp_dropped_source_count", "lfbp_hprime_device", "lfbp_hprime_host",
     "lfbp_hprime_multi", "lfbp_shard_planes", "lfbp_compare_device", "lfbp_plan_json",
-    "lfbp_launch_count", "lfbp_last_error", "lfbp_version",
+    "lfbp_launch_count", "lfbp_last_error", "lfbp_version", "lfbp_plane_sums_device",
 )
 
 _lock = threading.Lock()
@@ -43,6 +43,8 @@ _SIGS = {
     "lfbp_compare_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, _i64p,
                                            _i64p, ctypes.c_void_p]),
     "lfbp_plan_json": (ctypes.c_int, [_i64p, ctypes.c_int, ctypes.c_char_p, ctypes.c_int64]),
+    "lfbp_plane_sums_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64p, ctypes.c_int,
+                                              ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]),
     "lfbp_launch_count": (ctypes.c_int64, []),
     "lfbp_last_error": (ctypes.c_char_p, []),
     "lfbp_version": (ctypes.c_char_p, []),

@@ -25,6 +25,7 @@
 #include "../../include/lfbp_hprime.h"
 #include "hprime_kernel.cuh"
 #include "hprime_plan.h"
+#include "plane_sums.cuh"
 
 namespace {
 
@@ -794,6 +795,41 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
                    p.smem_bytes, p.ctas_per_sm, p.grid, (long long)p.n_units, p.sub_width, dp.sm_count,
                    dp.real ? "queried" : "b200-defaults", tuned ? "true" : "false");
   if (w < 0 || w >= buf_len) return fail(LFBP_ERR_ARGUMENT, "buffer too small");
+  return LFBP_OK;
+}
+
+int lfbp_plane_sums_device(const void* src, double* out, const int64_t dims[5], int dtype, int64_t z_begin,
+                           int64_t z_end, void* stream) {
+  int rc = check_common(dims, dtype, 0);
+  if (rc) return rc;
+  if (!src || !out) return fail(LFBP_ERR_ARGUMENT, "null device pointer");
+  if (z_begin < 0 || z_end > dims[4] || z_begin > z_end)
+    return fail(LFBP_ERR_ARGUMENT, "plane range [%lld, %lld) outside [0, %lld)", (long long)z_begin,
+                (long long)z_end, (long long)dims[4]);
+  const int64_t K = dims[2] * dims[3];
+  if (K > 8192) return fail(LFBP_ERR_UNSUPPORTED, "slice of %lld values exceeds the sort limit 8192", (long long)K);
+  int P = 32;
+  while (P < K) P <<= 1;
+  const int64_t n_slices = dims[0] * dims[1] * (z_end - z_begin);
+  if (n_slices == 0) return LFBP_OK;
+  int dev = 0;
+  HP_CUDA(cudaGetDevice(&dev));
+  const DevProps dp = device_props(dev);
+  const int wpc = int(std::max<int64_t>(1, std::min<int64_t>(8, (dp.smem_optin / 2) / (int64_t(P) * 8))));
+  const size_t smem = size_t(wpc) * P * 8;
+  const int64_t blocks = std::min<int64_t>((n_slices + wpc - 1) / wpc, int64_t(dp.sm_count) * 16);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == LFBP_F32) {
+    HP_CUDA(cudaFuncSetAttribute(hp::plane_sums_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    hp::plane_sums_kernel<float><<<int(blocks), 32 * wpc, smem, st>>>(
+        static_cast<const float*>(src), out, int32_t(dims[0]), int32_t(dims[1]), int32_t(K), P, z_begin, n_slices);
+  } else {
+    HP_CUDA(cudaFuncSetAttribute(hp::plane_sums_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    hp::plane_sums_kernel<double><<<int(blocks), 32 * wpc, smem, st>>>(
+        static_cast<const double*>(src), out, int32_t(dims[0]), int32_t(dims[1]), int32_t(K), P, z_begin, n_slices);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  HP_CUDA(cudaGetLastError());
   return LFBP_OK;
 }
 

@@ -96,3 +96,35 @@ def negative_control(hp) -> None:
     n_diff, first = compare_device(hp, bad)
     if n_diff != 1 or first != pos:
         raise VerificationFailure(f"negative control not caught: n_diff={n_diff} first={first} pos={pos}")
+
+
+def plane_sums_device(t, shape, z_range=None, stream=None):
+    """Sorted-order float64 sums of every (s, t) pattern slice (K3 kernel):
+    bit-identical to the reference's sum_forward_plane / sum_backward_plane
+    (arrays.py:211-239) for every plane.  Returns a CUDA float64 tensor of
+    shape (n_s, n_t, n_planes) in F layout."""
+    import torch
+
+    from .transform import _code_of
+    n_s, n_t, n_x, n_y, n_z = shape
+    z0, z1 = (0, n_z) if z_range is None else z_range
+    out = torch.empty((z1 - z0, n_t, n_s), dtype=torch.float64, device=t.device).permute(2, 1, 0)
+    if stream is None:
+        stream = torch.cuda.current_stream(t.device)
+    with torch.cuda.device(t.device):
+        rc = _native.lib().lfbp_plane_sums_device(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                                  _native.dims_array(shape), _code_of(t), int(z0), int(z1),
+                                                  ctypes.c_void_p(stream.cuda_stream))
+    _native.check(rc)
+    return out
+
+
+def rotation_check(h, hp, shape) -> int:
+    """Acceptance criterion 3 of the reference (test_acceptance.py:85-99) on
+    the device: sum_backward_plane(H') == rotate180(sum_forward_plane(H)) bit
+    for bit, every plane.  Returns the number of mismatching (s, t, z)."""
+    import torch
+    fwd = plane_sums_device(h, shape)
+    bwd = plane_sums_device(hp, shape)
+    rot = torch.flip(fwd, dims=(0, 1))
+    return int((bwd.contiguous().view(torch.int64) != rot.contiguous().view(torch.int64)).sum().item())

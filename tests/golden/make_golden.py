@@ -111,6 +111,12 @@ def make_small(path):
         bp = lfbp.compute_backprojection(psf)
         arrays[name + "__H"] = np.asfortranarray(H)
         arrays[name + "__Hp"] = np.asfortranarray(bp.data)
+        if kind not in ("bits32", "bits64"):   # PsfArray values: nonnegative, no NaN
+            # the reference's sorted-order plane sums (arrays.py:211-239), every plane
+            arrays[name + "__fwdsum"] = np.stack(
+                [lfbp.sum_forward_plane(psf, z) for z in range(1, shape[4] + 1)], axis=-1)
+            arrays[name + "__bwdsum"] = np.stack(
+                [lfbp.sum_backward_plane(bp, z) for z in range(1, shape[4] + 1)], axis=-1)
         odd = shape[0] % 2 == 1 and shape[1] % 2 == 1
         if odd:
             inv = lfbp.compute_psf_from_backprojection(lfbp.BackprojArray._wrap(dims, np.asfortranarray(H)))

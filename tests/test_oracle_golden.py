@@ -132,3 +132,33 @@ def test_oracle_matches_reference_digest_c2_planes():
         plane = baseline_plane(w, z)
         got = hprime_oracle(plane[..., None])
         assert hashlib.sha256(got.tobytes(order="F")).hexdigest() == d["hprime_plane_sha256"][z]
+
+
+def test_plane_sums_oracle_matches_reference(golden_small):
+    """Sorted-order plane sums (arrays.py:211-239) reproduce the reference's
+    sum_forward_plane / sum_backward_plane bit for bit, and the spelled-out
+    pairwise order (the K3 kernel's) equals numpy's."""
+    from oracle.plane_sums import pairwise_sum, plane_sums_oracle
+    cases, arrays = golden_small
+    n = 0
+    for c in cases:
+        key = c["name"] + "__fwdsum"
+        if key not in arrays:
+            continue
+        n += 1
+        H, Hp = arrays[c["name"] + "__H"], arrays[c["name"] + "__Hp"]
+        assert plane_sums_oracle(H).tobytes() == np.asfortranarray(arrays[key]).tobytes(), c["name"]
+        assert plane_sums_oracle(Hp).tobytes() == np.asfortranarray(arrays[c["name"] + "__bwdsum"]).tobytes()
+        s, t = H.shape[0] // 2, H.shape[1] // 3
+        want = arrays[key][s, t, 0]
+        assert pairwise_sum(np.sort(H[s, t, :, :, 0], axis=None)) == want
+    assert n >= 20
+
+
+def test_pairwise_order_long_slices():
+    from oracle.plane_sums import pairwise_sum
+    rng = np.random.default_rng(3)
+    for k in (1, 7, 8, 9, 127, 128, 129, 255, 441, 1000, 5225):
+        v = np.sort(rng.random(k).astype(np.float32) * rng.random(k).astype(np.float32) ** 7)
+        want = v.reshape(1, 1, k).sum(axis=-1, dtype=np.float64)[0, 0]
+        assert pairwise_sum(v) == want, k
