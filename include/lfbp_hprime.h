@@ -23,6 +23,8 @@
  *                             bench.py:88 / cli.py:145-150, on the device
  *   lfbp_plane_sums_device -> sum_forward_plane / sum_backward_plane
  *                             arrays.py:211-239 (acceptance criterion 3)
+ *   lfbp_lf5_*             -> read_lf5 / save / load_psf (fileio.py:46-113)
+ *                             and the `lfbp transform` CLI (cli.py:115-126)
  * Error codes mirror the reference's exceptions (errors.py:12-13, 32-33).
  */
 #ifndef LFBP_HPRIME_H
@@ -41,6 +43,9 @@ extern "C" {
 #define LFBP_ERR_CUDA 3             /* CUDA runtime failure; see lfbp_last_error() */
 #define LFBP_ERR_ARGUMENT 4         /* null / misaligned pointer, bad dtype or range */
 #define LFBP_ERR_UNSUPPORTED 5      /* shape beyond the kernel's limits */
+#define LFBP_ERR_FORMAT 6           /* lfbp.FormatError   (errors.py:20-21): malformed LF5 file */
+#define LFBP_ERR_IO 7               /* lfbp.IoError       (errors.py:24-25): read/write failed */
+#define LFBP_ERR_DIMS 8             /* lfbp.DimsError     (errors.py:16-17): file dims violate the contract */
 
 /* element type codes: the LF5 header codes (fileio.py:35) */
 #define LFBP_F32 1
@@ -101,6 +106,28 @@ int lfbp_compare_device(const void* a, const void* b, int64_t nbytes, int64_t* n
  * `stream`.  n_x*n_y must be <= 8192. */
 int lfbp_plane_sums_device(const void* src, double* out, const int64_t dims[5], int dtype, int64_t z_begin,
                            int64_t z_end, void* stream);
+
+/* ---- LF5 container streaming (fileio.py:3-92; 32-byte header + F-order payload) ---- */
+
+/* Parse and validate an LF5 header like read_lf5 (fileio.py:63-92): magic,
+ * version 1, element code, zero reserved bytes, exact file length.  No GPU. */
+int lfbp_lf5_read_header(const char* path, int64_t dims[5], int* dtype);
+
+/* Create / truncate `path` as an LF5 file of that shape and type (header
+ * written, payload sized).  No GPU. */
+int lfbp_lf5_create(const char* path, const int64_t dims[5], int dtype);
+
+/* File-to-file H' (inverse = 0) or H (inverse = 1): the `lfbp transform`
+ * CLI (cli.py:115-126) without holding the array in host memory -- plane
+ * chunks are pread into pinned buffers, transformed on `device` and pwritten
+ * at their offsets.  Header dims are checked like load_psf (DimsError), the
+ * values like PsfArray (InvalidDims for negative / NaN; no output is left). */
+int lfbp_lf5_transform_file(const char* in_path, const char* out_path, int inverse, int device, int flags);
+
+/* Planes [z_begin, z_end) of an LF5 file straight into / out of a device
+ * buffer that holds exactly those planes (z-sharded loads / stores). */
+int lfbp_lf5_load_device(const char* path, void* dst, int64_t z_begin, int64_t z_end, void* stream);
+int lfbp_lf5_store_device(const char* path, const void* src, int64_t z_begin, int64_t z_end, void* stream);
 
 /* The launch plan the kernel would use, as a JSON object in `buf` (for
  * tests, tuning and DESIGN.md).  Uses the current device's properties, or

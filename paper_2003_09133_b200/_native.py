@@ -10,11 +10,12 @@ import ctypes
 import os
 import threading
 
-from .errors import EvenPixelDims, InvalidDims, LfbpError, NativeError
+from .errors import DimsError, EvenPixelDims, FormatError, InvalidDims, IoError, LfbpError, NativeError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhprime.so")
 
-OK, ERR_INVALID_DIMS, ERR_EVEN_PIXEL_DIMS, ERR_CUDA, ERR_ARGUMENT, ERR_UNSUPPORTED = range(6)
+(OK, ERR_INVALID_DIMS, ERR_EVEN_PIXEL_DIMS, ERR_CUDA, ERR_ARGUMENT, ERR_UNSUPPORTED, ERR_FORMAT, ERR_IO,
+ ERR_DIMS) = range(9)
 F32, F64 = 1, 2
 HOST_REGISTER = 1
 HOST_STAGE = 2
@@ -23,6 +24,8 @@ EXPORTS = (
     "lfbp_check_dims", "lfbp_dropped_source_count", "lfbp_hprime_device", "lfbp_hprime_host",
     "lfbp_hprime_multi", "lfbp_shard_planes", "lfbp_compare_device", "lfbp_plan_json",
     "lfbp_launch_count", "lfbp_last_error", "lfbp_version", "lfbp_plane_sums_device",
+    "lfbp_lf5_read_header", "lfbp_lf5_create", "lfbp_lf5_transform_file", "lfbp_lf5_load_device",
+    "lfbp_lf5_store_device",
 )
 
 _lock = threading.Lock()
@@ -45,6 +48,14 @@ _SIGS = {
     "lfbp_plan_json": (ctypes.c_int, [_i64p, ctypes.c_int, ctypes.c_char_p, ctypes.c_int64]),
     "lfbp_plane_sums_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, _i64p, ctypes.c_int,
                                               ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p]),
+    "lfbp_lf5_read_header": (ctypes.c_int, [ctypes.c_char_p, _i64p, ctypes.POINTER(ctypes.c_int)]),
+    "lfbp_lf5_create": (ctypes.c_int, [ctypes.c_char_p, _i64p, ctypes.c_int]),
+    "lfbp_lf5_transform_file": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                               ctypes.c_int]),
+    "lfbp_lf5_load_device": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_void_p]),
+    "lfbp_lf5_store_device": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                             ctypes.c_void_p]),
     "lfbp_launch_count": (ctypes.c_int64, []),
     "lfbp_last_error": (ctypes.c_char_p, []),
     "lfbp_version": (ctypes.c_char_p, []),
@@ -90,6 +101,12 @@ def check(rc: int, invalid=InvalidDims, even=EvenPixelDims) -> None:
         raise even(msg)
     if rc == ERR_CUDA:
         raise NativeError(msg)
+    if rc == ERR_FORMAT:
+        raise FormatError(msg)
+    if rc == ERR_IO:
+        raise IoError(msg)
+    if rc == ERR_DIMS:
+        raise DimsError(msg)
     if rc in (ERR_ARGUMENT, ERR_UNSUPPORTED):
         raise LfbpError(msg) if rc == ERR_UNSUPPORTED else ValueError(msg)
     raise NativeError(f"status {rc}: {msg}")

@@ -332,13 +332,13 @@ int check_common(const int64_t dims[5], int dtype, int inverse) {
 
 int64_t plane_elems(const int64_t d[5]) { return d[0] * d[1] * d[2] * d[3]; }
 
-// ---- host memcpy thread pool (pageable <-> pinned staging) ----
-class CopyPool {
+// ---- host thread pool: parallel memcpy / pread / pwrite of staging chunks ----
+class HostPool {
  public:
-  explicit CopyPool(int n) {
+  explicit HostPool(int n) {
     for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { run(i); });
   }
-  ~CopyPool() {
+  ~HostPool() {
     {
       std::lock_guard<std::mutex> lk(mu_);
       stop_ = true;
@@ -346,21 +346,27 @@ class CopyPool {
     cv_.notify_all();
     for (auto& t : th_) t.join();
   }
-  // memcpy(dst, src, n) split over all workers; returns when done
-  void copy(void* dst, const void* src, size_t n) {
-    if (n < (size_t(4) << 20) || th_.empty()) {
-      memcpy(dst, src, n);
+  // fn(a, b) over [0, n) split into one part per worker (parts aligned to
+  // `align` bytes); returns when every part is done
+  void for_range(size_t n, size_t align, const std::function<void(size_t, size_t)>& fn) {
+    if (th_.empty() || n < (size_t(4) << 20)) {
+      fn(0, n);
       return;
     }
     std::lock_guard<std::mutex> one_job(call_mu_);  // callers from several device threads take turns
     std::unique_lock<std::mutex> lk(mu_);
-    dst_ = static_cast<uint8_t*>(dst);
-    src_ = static_cast<const uint8_t*>(src);
+    fn_ = &fn;
     n_ = n;
+    align_ = align;
     pending_ = int(th_.size());
     ++gen_;
     cv_.notify_all();
     done_.wait(lk, [this] { return pending_ == 0; });
+  }
+  void copy(void* dst, const void* src, size_t n) {
+    uint8_t* d = static_cast<uint8_t*>(dst);
+    const uint8_t* s = static_cast<const uint8_t*>(src);
+    for_range(n, 64, [&](size_t a, size_t b) { memcpy(d + a, s + a, b - a); });
   }
 
  private:
@@ -372,12 +378,11 @@ class CopyPool {
       if (stop_) return;
       seen = gen_;
       const size_t parts = th_.size();
-      const size_t chunk = (n_ / parts + 63) & ~size_t(63);
+      const size_t chunk = ((n_ / parts) + align_ - 1) / align_ * align_;
       const size_t a = std::min(n_, chunk * i), b = std::min(n_, a + chunk);
-      uint8_t* d = dst_;
-      const uint8_t* s = src_;
+      const std::function<void(size_t, size_t)>* fn = fn_;
       lk.unlock();
-      if (b > a) memcpy(d + a, s + a, b - a);
+      if (b > a) (*fn)(a, b);
       lk.lock();
       if (--pending_ == 0) done_.notify_one();
     }
@@ -386,16 +391,15 @@ class CopyPool {
   std::mutex call_mu_;
   std::mutex mu_;
   std::condition_variable cv_, done_;
-  uint8_t* dst_ = nullptr;
-  const uint8_t* src_ = nullptr;
-  size_t n_ = 0;
+  const std::function<void(size_t, size_t)>* fn_ = nullptr;
+  size_t n_ = 0, align_ = 64;
   int pending_ = 0;
   uint64_t gen_ = 0;
   bool stop_ = false;
 };
 
-CopyPool& copy_pool() {
-  static CopyPool pool(std::max(1, std::min(16, env_int("LFBP_COPY_THREADS",
+HostPool& copy_pool() {
+  static HostPool pool(std::max(1, std::min(16, env_int("LFBP_COPY_THREADS",
                                                         int(std::thread::hardware_concurrency()) / 2))));
   return pool;
 }
@@ -508,9 +512,29 @@ int maybe_pin(HostPin& pin, const void* p, size_t bytes, int flags) {
   return LFBP_OK;
 }
 
-// planes [z0, z1) of host src -> host dst through device `dev`
+// Optional hooks of the host pipeline: where a chunk's input comes from and
+// where its output goes when it is not a host array (the LF5 file path).
+// Offsets are byte offsets of the chunk in the whole array.
+using FillFn = std::function<int(uint8_t* pinned, int64_t off, size_t bytes)>;
+using FlushFn = std::function<int(const uint8_t* pinned, int64_t off, size_t bytes)>;
+
+// K4: elements failing `v >= 0` (negative or NaN), the reference's PsfArray
+// value check (arrays.py:106-107), counted on the device
+template <typename T>
+__global__ void count_invalid_kernel(const T* __restrict__ a, int64_t n, unsigned long long* count) {
+  unsigned long long c = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    c += !(a[i] >= T(0));
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+// planes [z0, z1) of host src -> host dst through device `dev`; with `fill`
+// / `flush` the chunks are produced / consumed by the hooks instead; with
+// `invalid` (device counter) the input values are checked like PsfArray's
 int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, int dev, int64_t z0, int64_t z1,
-              int flags) {
+              int flags, const FillFn* fill = nullptr, const FlushFn* flush = nullptr,
+              unsigned long long* invalid = nullptr) {
   HP_CUDA(cudaSetDevice(dev));
   const int64_t pb = plane_elems(dims) * E;
   const int64_t nz = z1 - z0;
@@ -520,8 +544,8 @@ int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, in
   const int64_t n_chunks = (nz + cp - 1) / cp;
   // pageable arrays: stage through pinned buffers (parallel host memcpy
   // overlapped with the DMA), or pin them in place, or let the driver stage
-  const bool stage_in = (flags & LFBP_HOST_STAGE) && !is_pinned(src + z0 * pb);
-  const bool stage_out = (flags & LFBP_HOST_STAGE) && !is_pinned(dst + z0 * pb);
+  const bool stage_in = fill || ((flags & LFBP_HOST_STAGE) && !is_pinned(src + z0 * pb));
+  const bool stage_out = flush || ((flags & LFBP_HOST_STAGE) && !is_pinned(dst + z0 * pb));
   const int reg_flags = flags & LFBP_HOST_REGISTER;
   HostPin pin_in, pin_out;
   int rc = stage_in ? LFBP_OK : maybe_pin(pin_in, src + z0 * pb, size_t(nz * pb), reg_flags);
@@ -540,12 +564,13 @@ int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, in
     a = z0 + c * cp;
     bytes = size_t(std::min<int64_t>(cp, z1 - a) * pb);
   };
-  auto drain = [&](int64_t c) -> int {  // staged output of chunk c -> dst
+  auto drain = [&](int64_t c) -> int {  // staged output of chunk c -> dst / flush hook
     int64_t a;
     size_t bytes;
     chunk_range(c, a, bytes);
     const int k = int(c % kPipe);
     HP_CUDA(cudaEventSynchronize(w.d2h_done[k]));
+    if (flush) return (*flush)(static_cast<const uint8_t*>(w.pin_out[k]), a * pb, bytes);
     copy_pool().copy(dst + a * pb, w.pin_out[k], bytes);
     return LFBP_OK;
   };
@@ -555,10 +580,15 @@ int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, in
     size_t bytes;
     chunk_range(c, a, bytes);
     const int64_t planes = int64_t(bytes) / pb;
-    const uint8_t* h_src = src + a * pb;
+    const uint8_t* h_src = src ? src + a * pb : nullptr;
     if (stage_in) {
       if (c >= kPipe) HP_CUDA(cudaEventSynchronize(w.h2d_done[k]));  // pin_in[k] free
-      copy_pool().copy(w.pin_in[k], h_src, bytes);
+      if (fill) {
+        rc = (*fill)(static_cast<uint8_t*>(w.pin_in[k]), a * pb, bytes);
+        if (rc) return rc;
+      } else {
+        copy_pool().copy(w.pin_in[k], h_src, bytes);
+      }
       h_src = static_cast<const uint8_t*>(w.pin_in[k]);
     }
     if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_h2d, w.cmp_done[k], 0));  // in[k] consumed
@@ -566,6 +596,16 @@ int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, in
     HP_CUDA(cudaEventRecord(w.h2d_done[k], w.s_h2d));
     HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.h2d_done[k], 0));
     if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.d2h_done[k], 0));  // out[k] drained
+    if (invalid) {
+      const int64_t n = int64_t(bytes) / E;
+      const int blocks = int(std::min<int64_t>(1184, (n + 255) / 256));
+      if (E == 4)
+        count_invalid_kernel<float><<<blocks, 256, 0, w.s_cmp>>>(static_cast<const float*>(w.in[k]), n, invalid);
+      else
+        count_invalid_kernel<double><<<blocks, 256, 0, w.s_cmp>>>(static_cast<const double*>(w.in[k]), n, invalid);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      HP_CUDA(cudaGetLastError());
+    }
     int64_t cd[5] = {dims[0], dims[1], dims[2], dims[3], planes};
     Knobs kn;
     if (!env_knobs_set()) tuned_knobs(TuneKey{dims[0], dims[1], dims[2], dims[3], E, dev}, kn);
@@ -800,8 +840,10 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
 
 int lfbp_plane_sums_device(const void* src, double* out, const int64_t dims[5], int dtype, int64_t z_begin,
                            int64_t z_end, void* stream) {
-  int rc = check_common(dims, dtype, 0);
-  if (rc) return rc;
+  // any positive shape (the reference sums unchecked-dims arrays too, fileio.py:95-104)
+  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || dims[3] < 1 || dims[4] < 1)
+    return fail(LFBP_ERR_INVALID_DIMS, "dims must all be >= 1");
+  if (!elem_size(dtype)) return fail(LFBP_ERR_ARGUMENT, "dtype code %d is not 1 (f32) or 2 (f64)", dtype);
   if (!src || !out) return fail(LFBP_ERR_ARGUMENT, "null device pointer");
   if (z_begin < 0 || z_end > dims[4] || z_begin > z_end)
     return fail(LFBP_ERR_ARGUMENT, "plane range [%lld, %lld) outside [0, %lld)", (long long)z_begin,
@@ -840,3 +882,5 @@ const char* lfbp_last_error(void) { return g_err.c_str(); }
 const char* lfbp_version(void) { return "lfbp-b200 0.1.0 (sm_100a)"; }
 
 }  // extern "C"
+
+#include "lf5_stream.inc"

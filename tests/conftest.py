@@ -33,3 +33,10 @@ def load_digests(cfg):
         return None
     with open(path) as f:
         return json.load(f)
+
+
+@pytest.fixture(scope="session")
+def golden_lf5():
+    import json
+    with open(os.path.join(GOLDEN, "small_cases.json")) as f:
+        return json.load(f)["lf5"]

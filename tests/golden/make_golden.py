@@ -124,10 +124,22 @@ def make_small(path):
         manifest.append({"name": name, "shape": list(shape), "dtype": np.dtype(dtype).name,
                          "kind": kind, "density": density, "seed": seed, "inverse": odd,
                          "dropped": int(lfbp.dropped_source_count(dims))})
+    # LF5 files written by the reference: input and `lfbp transform` output
+    import tempfile
+    lf5 = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name in ("rand_19_11_9_5_2", "rand_21_21_11_11_3", "even_10_5_5_5_2", "rand_5_5_3_3_1_f32"):
+            H = arrays[name + "__H"]
+            dims = Dims5(*H.shape)
+            fin, fout = os.path.join(td, "in.lf5"), os.path.join(td, "out.lf5")
+            lfbp.save(lfbp.PsfArray(dims, H), fin)
+            lfbp.save(lfbp.compute_backprojection(lfbp.load_psf(fin)), fout)
+            lf5[name] = {"in_sha256": hashlib.sha256(open(fin, "rb").read()).hexdigest(),
+                         "out_sha256": hashlib.sha256(open(fout, "rb").read()).hexdigest()}
     np.savez_compressed(path, **arrays)
     with open(path.replace(".npz", ".json"), "w") as f:
         json.dump({"generator": "tests/golden/make_golden.py", "reference": "lfbp " + lfbp.__version__,
-                   "numpy": np.__version__, "cases": manifest}, f, indent=1)
+                   "numpy": np.__version__, "cases": manifest, "lf5": lf5}, f, indent=1)
     print(f"wrote {path}: {len(manifest)} cases")
 
 

@@ -50,7 +50,8 @@ def test_plane_sums_match_reference_golden(golden_small):
 
 
 @pytest.mark.parametrize("shape,dtype", [((95, 55, 95, 55, 1), np.float32), ((17, 13, 11, 13, 3), np.float64),
-                                         ((9, 7, 31, 17, 2), np.float32), ((3, 3, 1, 1, 4), np.float32)])
+                                         ((9, 7, 31, 17, 2), np.float32), ((3, 3, 1, 1, 4), np.float32),
+                                         ((4, 6, 2, 2, 2), np.float64)])
 def test_plane_sums_match_oracle_random(shape, dtype):
     _torch()
     from paper_2003_09133_b200.synth import random_psf_like_reference
