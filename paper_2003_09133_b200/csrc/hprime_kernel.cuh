@@ -280,9 +280,18 @@ __device__ __forceinline__ void row_groups(typename Word<E>::T* o, int32_t g, in
     g += W;
   }
   const int32_t g_hi = last_full ? ng : ng - 1;
-  for (; g < g_hi; g += W) {
+  if (g < g_hi) {  // full groups, software-pipelined: load group k+1 before storing group k
     T v[VE];
     load_group<E, WRAP1>(v, a0, x0, n_x, step, nr);
+    for (g += W; g < g_hi; g += W) {
+      T* o_cur = o;
+      advance();
+      T vn[VE];
+      load_group<E, WRAP1>(vn, a0, x0, n_x, step, nr);
+      st_vec<E>(o_cur, v);
+#pragma unroll
+      for (int q = 0; q < VE; ++q) v[q] = vn[q];
+    }
     st_vec<E>(o, v);
     advance();
   }
@@ -309,8 +318,9 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
   const int32_t n_x = static_cast<int32_t>(p.n_x);
   const int32_t n_s = static_cast<int32_t>(p.n_s);
   const int32_t W = p.sub_width;
+  const int32_t lw = W == 8 ? 3 : W == 16 ? 4 : 5;  // log2(W): no integer division below
   const int32_t sl = lane & (W - 1);               // lane within the sub-warp
-  const int32_t R = 32 / W;                        // rows in flight per warp
+  const int32_t R = 32 >> lw;                      // rows in flight per warp
   const int32_t rp = p.row_pitch;
   const int32_t step = rp - E;                     // x -> x+1, s -> s-1
   const int32_t nr = n_x * rp;                     // ... minus this when x wraps to 0
@@ -324,13 +334,15 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
   T* dz = reinterpret_cast<T*>(dst) + h.plane_off;
   int* next_row = &reinterpret_cast<UnitHdr*>(const_cast<uint8_t*>(stage))->next_row;
   const int32_t rows = h.jb * n_x;
+  // rows are claimed R at a time (dynamic balance across warps); the next
+  // claim is issued before the current rows are written
+  int32_t claim = 0;
+  if (lane == 0) claim = atomicAdd(next_row, R);
   for (;;) {
-    // claim the next R rows of the unit (dynamic balance across warps)
-    int32_t r0 = 0;
-    if (lane == 0) r0 = atomicAdd(next_row, R);
-    r0 = __shfl_sync(0xffffffffu, r0, 0);
+    const int32_t r0 = __shfl_sync(0xffffffffu, claim, 0);
     if (r0 >= rows) break;
-    const int32_t r = r0 + lane / W;
+    if (lane == 0) claim = atomicAdd(next_row, R);
+    const int32_t r = r0 + (lane >> lw);
     do {  // this sub-warp's row (none past the end of the unit)
     if (r >= rows) break;
     const int32_t tl = static_cast<int32_t>(hp_div(p.nx_div, static_cast<uint32_t>(r)));
