@@ -25,6 +25,10 @@
  *                             arrays.py:211-239 (acceptance criterion 3)
  *   lfbp_lf5_*             -> read_lf5 / save / load_psf (fileio.py:46-113)
  *                             and the `lfbp transform` CLI (cli.py:115-126)
+ *   lfbp_forward_project_device / lfbp_backproject_device /
+ *   lfbp_safe_divide_device -> forward_project / backproject(_adjoint) /
+ *                             _safe_divide, projector.py:55-145 (the H'
+ *                             consumer; rl_run composes them)
  * Error codes mirror the reference's exceptions (errors.py:12-13, 32-33).
  */
 #ifndef LFBP_HPRIME_H
@@ -128,6 +132,26 @@ int lfbp_lf5_transform_file(const char* in_path, const char* out_path, int inver
  * buffer that holds exactly those planes (z-sharded loads / stores). */
 int lfbp_lf5_load_device(const char* path, void* dst, int64_t z_begin, int64_t z_end, void* stream);
 int lfbp_lf5_store_device(const char* path, const void* src, int64_t z_begin, int64_t z_end, void* stream);
+
+/* ---- the H' consumer (projector.py:55-145), float64 accumulation ----
+ * Volumes (nvx, nvy, n_z) and images (nvx, nvy) are F-ordered float64 device
+ * arrays; the pattern arrays H / H' are float32 or float64 (dtype code). */
+
+/* image = forward projection of the volume through H (projector.py:55-81). */
+int lfbp_forward_project_device(const void* H, int dtype, const int64_t dims[5], const double* volume, int64_t nvx,
+                                int64_t nvy, double* image, void* stream);
+
+/* volume = backprojection of the image: through H' stamps (use_hprime = 1,
+ * `backproject`, projector.py:103-126) or the literal adjoint through H
+ * (use_hprime = 0, `backproject_adjoint`, projector.py:84-100). */
+int lfbp_backproject_device(const void* P, int dtype, const int64_t dims[5], int use_hprime, const double* image,
+                            int64_t npx, int64_t npy, double* volume, void* stream);
+
+/* out = num / den where den >= eps * max(den) (and den > 0 if that is 0),
+ * else 0 (`_safe_divide`, projector.py:135-145); `scratch` is one device
+ * double. */
+int lfbp_safe_divide_device(const double* num, const double* den, double* out, int64_t n, double eps,
+                            double* scratch, void* stream);
 
 /* The launch plan the kernel would use, as a JSON object in `buf` (for
  * tests, tuning and DESIGN.md).  Uses the current device's properties, or

@@ -25,7 +25,8 @@ EXPORTS = (
     "lfbp_hprime_multi", "lfbp_shard_planes", "lfbp_compare_device", "lfbp_plan_json",
     "lfbp_launch_count", "lfbp_last_error", "lfbp_version", "lfbp_plane_sums_device",
     "lfbp_lf5_read_header", "lfbp_lf5_create", "lfbp_lf5_transform_file", "lfbp_lf5_load_device",
-    "lfbp_lf5_store_device",
+    "lfbp_lf5_store_device", "lfbp_forward_project_device", "lfbp_backproject_device",
+    "lfbp_safe_divide_device",
 )
 
 _lock = threading.Lock()
@@ -56,6 +57,12 @@ _SIGS = {
                                             ctypes.c_void_p]),
     "lfbp_lf5_store_device": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
                                              ctypes.c_void_p]),
+    "lfbp_forward_project_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _i64p, ctypes.c_void_p,
+                                                   ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "lfbp_backproject_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _i64p, ctypes.c_int, ctypes.c_void_p,
+                                               ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "lfbp_safe_divide_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                               ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
     "lfbp_launch_count": (ctypes.c_int64, []),
     "lfbp_last_error": (ctypes.c_char_p, []),
     "lfbp_version": (ctypes.c_char_p, []),

@@ -26,6 +26,7 @@
 #include "hprime_kernel.cuh"
 #include "hprime_plan.h"
 #include "plane_sums.cuh"
+#include "projector.cuh"
 
 namespace {
 
@@ -117,8 +118,8 @@ bool env_knobs_set() {
 // Candidates tried by the autotuner (measured best plans of C1..C5 and
 // neighbours; every one is bit-exact, they differ only in speed).
 const Knobs kCandidates[] = {
-    {3, 48, 8, 8},   {3, 48, 16, 16}, {4, 48, 8, 16}, {4, 32, 16, 32},
-    {4, 48, 16, 32}, {3, 48, 8, 32},  {2, 48, 4, 8},  {4, 32, 8, 16},
+    {3, 48, 8, 8},  {4, 48, 12, 16}, {4, 48, 8, 8},  {4, 48, 8, 16},
+    {4, 32, 8, 16}, {3, 64, 8, 32},  {4, 48, 16, 16}, {4, 32, 4, 8},
 };
 
 // Work-unit shape, smem ring and persistent grid for one launch.
@@ -871,6 +872,72 @@ int lfbp_plane_sums_device(const void* src, double* out, const int64_t dims[5], 
         static_cast<const double*>(src), out, int32_t(dims[0]), int32_t(dims[1]), int32_t(K), P, z_begin, n_slices);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  HP_CUDA(cudaGetLastError());
+  return LFBP_OK;
+}
+
+static int proj_geom(hp::ProjGeom& q, const int64_t dims[5], int64_t nvx, int64_t nvy) {
+  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || dims[3] < 1 || dims[4] < 1 || nvx < 1 || nvy < 1)
+    return fail(LFBP_ERR_INVALID_DIMS, "bad projector geometry");
+  if (dims[0] * dims[1] * dims[2] * dims[3] >= (int64_t(1) << 31) || nvx * nvy >= (int64_t(1) << 31))
+    return fail(LFBP_ERR_UNSUPPORTED, "projector plane too large");
+  q.n_s = int32_t(dims[0]);
+  q.n_t = int32_t(dims[1]);
+  q.n_x = int32_t(dims[2]);
+  q.n_y = int32_t(dims[3]);
+  q.n_z = int32_t(dims[4]);
+  // pattern_centre (projector.py:26-32) minus one
+  q.c_s = int32_t(dims[0] % 2 ? (dims[0] + 1) / 2 - 1 : dims[0] / 2);
+  q.c_t = int32_t(dims[1] % 2 ? (dims[1] + 1) / 2 - 1 : dims[1] / 2);
+  q.nvx = int32_t(nvx);
+  q.nvy = int32_t(nvy);
+  return LFBP_OK;
+}
+
+int lfbp_forward_project_device(const void* H, int dtype, const int64_t dims[5], const double* volume, int64_t nvx,
+                                int64_t nvy, double* image, void* stream) {
+  hp::ProjGeom q;
+  int rc = proj_geom(q, dims, nvx, nvy);
+  if (rc) return rc;
+  if (!H || !volume || !image || !elem_size(dtype)) return fail(LFBP_ERR_ARGUMENT, "bad forward_project arguments");
+  const dim3 blk(32, 8), grd(unsigned((nvx + 31) / 32), unsigned((nvy + 7) / 8));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == LFBP_F32)
+    hp::forward_project_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(H), volume, image, q);
+  else
+    hp::forward_project_kernel<double><<<grd, blk, 0, st>>>(static_cast<const double*>(H), volume, image, q);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  HP_CUDA(cudaGetLastError());
+  return LFBP_OK;
+}
+
+int lfbp_backproject_device(const void* P, int dtype, const int64_t dims[5], int use_hprime, const double* image,
+                            int64_t npx, int64_t npy, double* volume, void* stream) {
+  hp::ProjGeom q;
+  int rc = proj_geom(q, dims, npx, npy);
+  if (rc) return rc;
+  if (!P || !volume || !image || !elem_size(dtype)) return fail(LFBP_ERR_ARGUMENT, "bad backproject arguments");
+  const dim3 blk(32, 8), grd(unsigned((npx + 31) / 32), unsigned((npy + 7) / 8), unsigned(dims[4]));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == LFBP_F32)
+    hp::backproject_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(P), image, volume, q, use_hprime);
+  else
+    hp::backproject_kernel<double><<<grd, blk, 0, st>>>(static_cast<const double*>(P), image, volume, q, use_hprime);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  HP_CUDA(cudaGetLastError());
+  return LFBP_OK;
+}
+
+int lfbp_safe_divide_device(const double* num, const double* den, double* out, int64_t n, double eps,
+                            double* scratch, void* stream) {
+  if (!num || !den || !out || !scratch || n < 0) return fail(LFBP_ERR_ARGUMENT, "bad safe_divide arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  HP_CUDA(cudaMemsetAsync(scratch, 0, sizeof(double), st));
+  if (n == 0) return LFBP_OK;
+  const int blocks = int(std::min<int64_t>(1184, (n + 255) / 256));
+  hp::max_kernel<<<blocks, 256, 0, st>>>(den, n, scratch);
+  hp::safe_divide_kernel<<<blocks, 256, 0, st>>>(num, den, out, n, eps, scratch);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
   HP_CUDA(cudaGetLastError());
   return LFBP_OK;
 }

@@ -1,0 +1,135 @@
+// The H' consumer on the GPU: forward and back
+// projection of the reference's light-field model (lfbp/projector.py:55-132),
+// float64 accumulation as in the reference.
+//
+// A voxel at (x, y, z) contributes its pattern H[:, :, x mod n_x, y mod n_y, z]
+// centred on the pixel under it (pattern element a lands on image row
+// S = x + a - C_s, C = pattern_centre - 1, projector.py:26-47); contributions
+// past the image border are dropped.  The reference scatters ("stamps") one
+// pattern per voxel / per pixel; here every output element GATHERS its own
+// window, one thread per output element, so no atomics are needed:
+//
+//   forward   out[S,T]    = sum_z sum_{a,b} g[S-a+C_s, T-b+C_t, z] *
+//                                        H[a, b, (S-a+C_s) mod n_x, (T-b+C_t) mod n_y, z]
+//   adjoint   out[x,y,z]  = sum_{S,T} f[S,T] * H[S-x+C_s, T-y+C_t, x mod n_x, y mod n_y, z]
+//   H'-stamp  out[X,Y,z]  = sum_{s,t} f[s,t] * H'[X-s+C_s, Y-t+C_t, s mod n_x, t mod n_y, z]
+//
+// (projector.py:55-81, 84-100, 103-126).  Sums run in a different order than
+// the reference's, so parity is to relative 1e-12 -- the tolerance the
+// reference's own tests use between its two backprojection forms
+// (test_projector.py:67-82).  All arrays are F-ordered; volumes / images are
+// float64.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hp {
+
+struct ProjGeom {
+  int32_t n_s, n_t, n_x, n_y, n_z;
+  int32_t c_s, c_t;      // pattern_centre - 1 (0-based zero-offset element)
+  int32_t nvx, nvy;      // lateral grid (image == volume lateral size)
+};
+
+template <typename T>
+__global__ void forward_project_kernel(const T* __restrict__ H, const double* __restrict__ g,
+                                       double* __restrict__ out, const ProjGeom q) {
+  const int32_t S = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t Tt = blockIdx.y * blockDim.y + threadIdx.y;
+  if (S >= q.nvx || Tt >= q.nvy) return;
+  const int64_t pat = int64_t(q.n_s) * q.n_t;
+  const int64_t plane = pat * q.n_x * q.n_y;
+  const int64_t vplane = int64_t(q.nvx) * q.nvy;
+  // pattern rows that keep the voxel inside the grid: 0 <= S - a + C < nvx
+  const int32_t a_lo = max(0, S + q.c_s - (q.nvx - 1)), a_hi = min(q.n_s - 1, S + q.c_s);
+  const int32_t b_lo = max(0, Tt + q.c_t - (q.nvy - 1)), b_hi = min(q.n_t - 1, Tt + q.c_t);
+  double acc = 0.0;
+  for (int32_t z = 0; z < q.n_z; ++z) {
+    const T* Hz = H + z * plane;
+    const double* gz = g + z * vplane;
+    for (int32_t b = b_lo; b <= b_hi; ++b) {
+      const int32_t y = Tt - b + q.c_t;
+      const int64_t yoff = int64_t(y % q.n_y) * q.n_x * pat + int64_t(b) * q.n_s;
+      const double* grow = gz + int64_t(y) * q.nvx;
+      for (int32_t a = a_lo; a <= a_hi; ++a) {
+        const int32_t x = S - a + q.c_s;
+        const double w = grow[x];
+        if (w != 0.0) acc = fma(w, static_cast<double>(Hz[yoff + int64_t(x % q.n_x) * pat + a]), acc);
+      }
+    }
+  }
+  out[S + int64_t(Tt) * q.nvx] = acc;
+}
+
+// adjoint (use_hprime = 0, pattern array H, voxel phase) or the H'-stamp
+// backprojection (use_hprime = 1, pattern array H', pixel phase)
+template <typename T>
+__global__ void backproject_kernel(const T* __restrict__ P, const double* __restrict__ f, double* __restrict__ out,
+                                   const ProjGeom q, int use_hprime) {
+  const int32_t X = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t Y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int32_t z = blockIdx.z;
+  if (X >= q.nvx || Y >= q.nvy) return;
+  const int64_t pat = int64_t(q.n_s) * q.n_t;
+  const T* Pz = P + z * pat * q.n_x * q.n_y;
+  double acc = 0.0;
+  if (use_hprime) {
+    // pixels s with 0 <= X - s + C_s < n_s
+    const int32_t s_lo = max(0, X + q.c_s - (q.n_s - 1)), s_hi = min(q.nvx - 1, X + q.c_s);
+    const int32_t t_lo = max(0, Y + q.c_t - (q.n_t - 1)), t_hi = min(q.nvy - 1, Y + q.c_t);
+    for (int32_t t = t_lo; t <= t_hi; ++t) {
+      const int32_t b = Y - t + q.c_t;
+      const int64_t toff = int64_t(t % q.n_y) * q.n_x * pat + int64_t(b) * q.n_s;
+      const double* frow = f + int64_t(t) * q.nvx;
+      for (int32_t s = s_lo; s <= s_hi; ++s) {
+        const double w = frow[s];
+        if (w != 0.0) acc = fma(w, static_cast<double>(Pz[toff + int64_t(s % q.n_x) * pat + (X - s + q.c_s)]), acc);
+      }
+    }
+  } else {
+    // pixels S with 0 <= S - X + C_s < n_s; the voxel's phase fixes the pattern
+    const int32_t S_lo = max(0, X - q.c_s), S_hi = min(q.nvx - 1, X - q.c_s + q.n_s - 1);
+    const int32_t T_lo = max(0, Y - q.c_t), T_hi = min(q.nvy - 1, Y - q.c_t + q.n_t - 1);
+    const T* Pxy = Pz + (int64_t(X % q.n_x) + int64_t(Y % q.n_y) * q.n_x) * pat;
+    for (int32_t Tt = T_lo; Tt <= T_hi; ++Tt) {
+      const T* prow = Pxy + int64_t(Tt - Y + q.c_t) * q.n_s;
+      const double* frow = f + int64_t(Tt) * q.nvx;
+      for (int32_t S = S_lo; S <= S_hi; ++S) acc = fma(frow[S], static_cast<double>(prow[S - X + q.c_s]), acc);
+    }
+  }
+  out[X + int64_t(Y) * q.nvx + int64_t(z) * q.nvx * q.nvy] = acc;
+}
+
+// _safe_divide (projector.py:135-145): num / den where den >= eps * max(den)
+// (and den > 0 when eps * max == 0), else 0; `peak` is max(den) on the device
+__global__ void safe_divide_kernel(const double* __restrict__ num, const double* __restrict__ den,
+                                   double* __restrict__ out, int64_t n, double eps, const double* __restrict__ peak) {
+  const double pk = *peak;
+  const double thr = eps * pk;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double r = 0.0;
+    if (pk > 0.0) {
+      const double d = den[i];
+      bool ok = d >= thr;
+      if (thr == 0.0) ok = ok && d > 0.0;
+      if (ok) r = num[i] / d;
+    }
+    out[i] = r;
+  }
+}
+
+__device__ __forceinline__ void atomic_max_double(double* a, double v) {
+  // nonnegative doubles order like their bit patterns; NaN / negatives never win
+  if (!(v > 0.0)) return;
+  atomicMax(reinterpret_cast<unsigned long long*>(a), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+__global__ void max_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ peak) {
+  double m = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    m = fmax(m, x[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomic_max_double(peak, m);
+}
+
+}  // namespace hp

@@ -54,14 +54,22 @@ def main():
                 for _ in range(3):
                     hprime_device(src, out=out)
                 torch.cuda.synchronize()
+                # time >= ~60 ms per variant (short windows are biased by clock / power transients)
+                t0 = torch.cuda.Event(enable_timing=True)
+                t1 = torch.cuda.Event(enable_timing=True)
+                t0.record()
+                hprime_device(src, out=out)
+                t1.record()
+                torch.cuda.synchronize()
+                reps = max(a.reps, int(60.0 / max(t0.elapsed_time(t1), 1e-3)))
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-                for _ in range(a.reps):
+                for _ in range(reps):
                     hprime_device(src, out=out)
                 e1.record()
                 torch.cuda.synchronize()
-                ms = e0.elapsed_time(e1) / a.reps
+                ms = e0.elapsed_time(e1) / reps
             except Exception as exc:  # noqa: BLE001
                 print(json.dumps({"config": cfg, "knobs": combo, "error": str(exc)}), flush=True)
                 continue
