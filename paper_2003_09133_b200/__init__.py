@@ -8,16 +8,16 @@ types and the ``InvalidDims`` / ``EvenPixelDims`` errors; plus the device
 API ``hprime_device`` and the z-slab launcher in ``shard``.
 """
 from .arrays import BackprojArray, Dims5, PsfArray
-from .errors import (DimsError, EvenPixelDims, FormatError, InvalidDims, IoError, LfbpError, NativeError,
-                     VerificationFailure)
+from .errors import (DimMismatch, DimsError, EvenPixelDims, FormatError, InvalidDims, IoError, LfbpError,
+                     NativeError, NonFiniteInput, VerificationFailure)
 from .transform import (compute_backprojection, compute_psf_from_backprojection, dropped_source_count,
                         f_order_empty, hprime_device, plan)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BackprojArray", "Dims5", "PsfArray", "DimsError", "EvenPixelDims", "FormatError", "InvalidDims",
-    "IoError", "LfbpError", "NativeError",
+    "BackprojArray", "Dims5", "PsfArray", "DimMismatch", "DimsError", "EvenPixelDims", "FormatError",
+    "InvalidDims", "IoError", "LfbpError", "NativeError", "NonFiniteInput",
     "VerificationFailure", "compute_backprojection", "compute_psf_from_backprojection",
     "dropped_source_count", "f_order_empty", "hprime_device", "plan",
 ]

@@ -143,6 +143,53 @@ def make_small(path):
     print(f"wrote {path}: {len(manifest)} cases")
 
 
+def make_projector(path):
+    """Reference projector outputs (projector.py:55-196) for the GPU f2 path."""
+    out = {}
+    rng = np.random.default_rng(17)
+    cases = []
+    # (name, psf, volume shape, image shape)
+    psf = lfbp.random_psf(Dims5(9, 9, 3, 3, 3), density=0.4, seed=17)
+    cases.append(("sym", psf, rng.random((31, 31, 3)), rng.random((31, 31))))
+    psf = lfbp.random_psf(Dims5(6, 6, 3, 5, 2), density=0.6, seed=6)
+    cases.append(("even", psf, rng.random((17, 19, 2)), rng.random((17, 19))))
+    psf = lfbp.random_psf(Dims5(19, 11, 9, 5, 2), density=0.5, seed=19)
+    cases.append(("asym", psf, rng.random((23, 29, 2)), rng.random((23, 29))))
+    psf = lfbp.random_psf(Dims5(5, 5, 3, 3, 1), density=1.0, seed=3, dtype=np.float32)
+    cases.append(("f32", psf, np.ones((9, 9, 1)), np.ones((9, 9))))
+    for name, psf, g, f in cases:
+        bp = lfbp.compute_backprojection(psf)
+        out[name + "__H"] = np.asfortranarray(psf.data)
+        out[name + "__g"] = np.asfortranarray(g)
+        out[name + "__f"] = np.asfortranarray(f)
+        out[name + "__fwd"] = lfbp.forward_project(psf, lfbp.Volume(g)).data
+        out[name + "__bp"] = lfbp.backproject(bp, lfbp.Image(f)).data
+        out[name + "__adj"] = lfbp.backproject_adjoint(psf, lfbp.Image(f)).data
+        out[name + "__norm"] = lfbp.normalizer(bp, f.shape).data
+    # RL: reference test_projector.py:140-150 and acceptance criterion 6
+    psf = lfbp.random_psf(Dims5(5, 5, 3, 3, 2), density=0.9, seed=15)
+    g = np.zeros((11, 11, 2)); g[5, 5, 0] = 1.0; g[2, 8, 1] = 0.5
+    img = lfbp.forward_project(psf, lfbp.Volume(g))
+    st = lfbp.rl_run(psf, lfbp.compute_backprojection(psf), img, iterations=6)
+    out["rl6__H"] = np.asfortranarray(psf.data)
+    out["rl6__f"] = img.data
+    out["rl6__est"] = st.estimate.data
+    out["rl6__mse"] = np.asarray(st.mse_history)
+    layout = lfbp.MlaLayout.rect(5.0)
+    optics = lfbp.SpotOptics(sigma=0.7, fnumber=4.0, z_step=3.0, sigma_gain=0.3, focal_plane=0)
+    psf = lfbp.synth_psf(layout, Dims5(17, 17, 5, 5, 3), optics)
+    g = np.zeros((31, 31, 3)); g[9, 11, 0] = 1.0; g[21, 19, 2] = 1.0
+    img = lfbp.forward_project(psf, lfbp.Volume(g))
+    st = lfbp.rl_run(psf, lfbp.compute_backprojection(psf), img, iterations=20)
+    out["rl20__H"] = np.asfortranarray(psf.data)
+    out["rl20__f"] = img.data
+    out["rl20__est"] = st.estimate.data
+    out["rl20__mse"] = np.asarray(st.mse_history)
+    out["rl20__dead"] = np.asarray(st.dead_voxels)
+    np.savez_compressed(path, **out)
+    print(f"wrote {path}: {len(out)} arrays")
+
+
 def make_digests(cfg: str, slab: int):
     w = WORKLOADS[cfg]
     n_s, n_t, n_x, n_y, n_z = w.shape
@@ -186,6 +233,7 @@ def main():
     a = ap.parse_args()
     if a.small:
         make_small(os.path.join(HERE, "small_cases.npz"))
+        make_projector(os.path.join(HERE, "projector_cases.npz"))
     for c in [c for c in a.configs.split(",") if c]:
         make_digests(c, a.slab)
 

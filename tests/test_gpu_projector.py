@@ -1,0 +1,171 @@
+"""The H' consumer on the GPU (f2; -m gpu): projections and Richardson-Lucy
+against the reference's outputs (tests/golden/projector_cases.npz) to the
+reference's own tolerance (relative 1e-12 between its two backprojection
+forms, test_projector.py:67-82), plus the reference's projector tests and
+acceptance criteria 5-6 restated."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import projector_oracle as po
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def proj():
+    return dict(np.load(os.path.join(GOLDEN, "projector_cases.npz")))
+
+
+def rel(a, b):
+    denom = np.maximum(np.abs(b), 1e-300)
+    return float(np.max(np.abs(a - b) / denom)) if a.size else 0.0
+
+
+def _arrays(H):
+    from paper_2003_09133_b200 import BackprojArray, Dims5, PsfArray, compute_backprojection
+    psf = PsfArray._wrap(Dims5.unchecked(*H.shape), H)
+    return psf, compute_backprojection(psf)
+
+
+@pytest.mark.parametrize("name", ["sym", "even", "asym", "f32"])
+def test_projections_match_reference(proj, name):
+    _torch()
+    from paper_2003_09133_b200.arrays import Image, Volume
+    from paper_2003_09133_b200.projector import backproject, backproject_adjoint, forward_project, normalizer
+    H, g, f = proj[name + "__H"], proj[name + "__g"], proj[name + "__f"]
+    psf, bp = _arrays(H)
+    fwd = forward_project(psf, Volume(g)).data
+    assert fwd.dtype == np.float64 and rel(fwd, proj[name + "__fwd"]) < 1e-12
+    assert rel(backproject(bp, Image(f)).data, proj[name + "__bp"]) < 1e-12
+    assert rel(backproject_adjoint(psf, Image(f)).data, proj[name + "__adj"]) < 1e-12
+    assert rel(normalizer(bp, f.shape).data, proj[name + "__norm"]) < 1e-12
+
+
+def test_reference_projector_kats():
+    """test_projector.py:19-58 restated: zero volume, one voxel stamps its
+    pattern exactly, border clipping, cell-shift equivariance."""
+    _torch()
+    from paper_2003_09133_b200 import Dims5, PsfArray
+    from paper_2003_09133_b200.arrays import Volume
+    from paper_2003_09133_b200.projector import forward_project, pattern_centre
+    from paper_2003_09133_b200.synth import random_psf_like_reference as rpsf
+    psf = PsfArray._wrap(Dims5(9, 9, 3, 3, 2), rpsf((9, 9, 3, 3, 2), seed=0))
+    img = forward_project(psf, Volume(np.zeros((15, 15, 2))))
+    assert img.shape == (15, 15) and not img.data.any()
+    H = rpsf((5, 5, 3, 3, 2), density=1.0, seed=8)
+    g = np.zeros((15, 15, 2)); g[7, 6, 1] = 2.0
+    img = forward_project(PsfArray._wrap(Dims5(5, 5, 3, 3, 2), H), Volume(g))
+    want = np.zeros((15, 15)); c = pattern_centre(5)
+    want[7 - (c - 1):7 + c, 6 - (c - 1):6 + c] = 2.0 * H[:, :, 7 % 3, 6 % 3, 1]
+    assert np.array_equal(img.data, want)
+    ones = PsfArray._wrap(Dims5(5, 5, 3, 3, 1), np.ones((5, 5, 3, 3, 1), order="F"))
+    g = np.zeros((7, 7, 1)); g[0, 0, 0] = 1.0
+    img = forward_project(ones, Volume(g))
+    assert img.data.sum() == 9.0 and np.count_nonzero(img.data) == 9
+    H = rpsf((9, 9, 3, 3, 1), density=0.8, seed=4)
+    psf = PsfArray._wrap(Dims5(9, 9, 3, 3, 1), H)
+    g1 = np.zeros((31, 31, 1)); g1[10, 12, 0] = 1.0
+    g2 = np.zeros((31, 31, 1)); g2[13, 12, 0] = 1.0
+    f1 = forward_project(psf, Volume(g1)).data
+    f2 = forward_project(psf, Volume(g2)).data
+    assert np.array_equal(f1[6:15, :], f2[9:18, :])
+
+
+def test_criterion_5_adjointness_on_gpu():
+    """<Hg, f> = <g, H'f> within 1e-10 and the H' path equals the literal
+    adjoint within 1e-12, 20 instances (test_acceptance.py:128-152)."""
+    _torch()
+    from paper_2003_09133_b200 import Dims5, PsfArray, compute_backprojection
+    from paper_2003_09133_b200.arrays import Image, Volume
+    from paper_2003_09133_b200.projector import backproject, backproject_adjoint, forward_project
+    from paper_2003_09133_b200.synth import random_psf_like_reference as rpsf
+    worst_rel = worst_pair = 0.0
+    for i in range(20):
+        psf = PsfArray._wrap(Dims5(9, 9, 3, 3, 3), rpsf((9, 9, 3, 3, 3), density=0.3, seed=2000 + i))
+        bp = compute_backprojection(psf)
+        rng = np.random.default_rng(3000 + i)
+        g = Volume(rng.random((31, 31, 3)))
+        f = Image(rng.random((31, 31)))
+        lhs = float(np.vdot(forward_project(psf, g).data, f.data))
+        via = backproject(bp, f).data
+        rhs = float(np.vdot(g.data, via))
+        worst_rel = max(worst_rel, abs(lhs - rhs) / abs(lhs))
+        worst_pair = max(worst_pair, rel(via, backproject_adjoint(psf, f).data))
+    assert worst_rel < 1e-10 and worst_pair < 1e-12
+
+
+def test_rl_matches_reference(proj):
+    _torch()
+    from paper_2003_09133_b200.arrays import Image
+    from paper_2003_09133_b200.projector import rl_run
+    psf, bp = _arrays(proj["rl6__H"])
+    st = rl_run(psf, bp, Image(proj["rl6__f"]), iterations=6)
+    assert st.iterations == 6 and len(st.mse_history) == 6
+    assert rel(st.estimate.data, proj["rl6__est"]) < 1e-9
+    assert np.allclose(st.mse_history, proj["rl6__mse"], rtol=1e-9, atol=0)
+    assert (st.estimate.data >= 0).all() and st.mse_history[-1] < st.mse_history[0]
+
+
+def test_criterion_6_rl_recovers_two_point_scene(proj):
+    """test_acceptance.py:155-180 on the GPU: top-2 voxels exact, MSE never
+    increases, and the estimate tracks the reference's."""
+    _torch()
+    from paper_2003_09133_b200.arrays import Image
+    from paper_2003_09133_b200.projector import rl_run
+    psf, bp = _arrays(proj["rl20__H"])
+    st = rl_run(psf, bp, Image(proj["rl20__f"]), iterations=20)
+    est = st.estimate.data
+    order = np.argsort(est.ravel())[::-1]
+    top = {tuple(int(i) for i in np.unravel_index(k, est.shape)) for k in order[:2]}
+    assert top == {(9, 11, 0), (21, 19, 2)}
+    assert sum(b > a for a, b in zip(st.mse_history, st.mse_history[1:])) == 0
+    assert st.dead_voxels == int(proj["rl20__dead"])
+    assert np.allclose(st.mse_history, proj["rl20__mse"], rtol=1e-6, atol=1e-18)
+
+
+def test_rl_zero_image_and_argument_checks():
+    _torch()
+    from paper_2003_09133_b200 import Dims5, DimMismatch, NonFiniteInput, PsfArray, compute_backprojection
+    from paper_2003_09133_b200.arrays import Image
+    from paper_2003_09133_b200.projector import rl_run
+    from paper_2003_09133_b200.synth import random_psf_like_reference as rpsf
+    psf = PsfArray._wrap(Dims5(5, 5, 3, 3, 1), rpsf((5, 5, 3, 3, 1), density=0.9, seed=5))
+    bp = compute_backprojection(psf)
+    st = rl_run(psf, bp, Image(np.zeros((9, 9))), iterations=3)
+    assert not st.estimate.data.any() and st.mse_history == [0.0, 0.0, 0.0]
+    with pytest.raises(ValueError):
+        rl_run(psf, bp, Image(np.zeros((9, 9))), iterations=0)
+    other = compute_backprojection(PsfArray._wrap(Dims5(7, 7, 3, 3, 1), rpsf((7, 7, 3, 3, 1), seed=1)))
+    with pytest.raises(DimMismatch):
+        rl_run(psf, other, Image(np.zeros((9, 9))), iterations=1)
+    with pytest.raises(NonFiniteInput):
+        rl_run(psf, bp, Image._wrap(np.full((9, 9), np.inf)), iterations=1)
+
+
+@pytest.mark.parametrize("shape,img", [((15, 13, 5, 3, 2), (40, 33)), ((55, 55, 11, 11, 2), (121, 99)),
+                                       ((8, 12, 7, 3, 2), (20, 17))])
+def test_random_shapes_match_oracle(shape, img):
+    _torch()
+    from paper_2003_09133_b200 import Dims5, PsfArray, compute_backprojection
+    from paper_2003_09133_b200.arrays import Image, Volume
+    from paper_2003_09133_b200.projector import backproject, backproject_adjoint, forward_project
+    from paper_2003_09133_b200.synth import random_psf_like_reference as rpsf
+    H = rpsf(shape, density=0.5, seed=3, dtype=np.float32)
+    psf = PsfArray._wrap(Dims5(*shape), H)
+    bp = compute_backprojection(psf)
+    rng = np.random.default_rng(4)
+    g = rng.random((*img, shape[4]))
+    f = rng.random(img)
+    assert rel(forward_project(psf, Volume(g)).data, po.forward_project(H, g)) < 1e-12
+    assert rel(backproject(bp, Image(f)).data, po.backproject(bp.data, f)) < 1e-12
+    assert rel(backproject_adjoint(psf, Image(f)).data, po.backproject_adjoint(H, f)) < 1e-12
