@@ -141,6 +141,12 @@ int lfbp_lf5_store_device(const char* path, const void* src, int64_t z_begin, in
 int lfbp_forward_project_device(const void* H, int dtype, const int64_t dims[5], const double* volume, int64_t nvx,
                                 int64_t nvy, double* image, void* stream);
 
+/* The same through H' when it is given and n_s, n_t are odd: each pixel's
+ * own phase fixes the pattern (coalesced gather, same sums); H may be NULL
+ * then.  Falls back to H for even sizes. */
+int lfbp_forward_project2_device(const void* H, const void* Hp, int dtype, const int64_t dims[5], const double* volume,
+                                 int64_t nvx, int64_t nvy, double* image, void* stream);
+
 /* volume = backprojection of the image: through H' stamps (use_hprime = 1,
  * `backproject`, projector.py:103-126) or the literal adjoint through H
  * (use_hprime = 0, `backproject_adjoint`, projector.py:84-100). */

@@ -26,7 +26,7 @@ EXPORTS = (
     "lfbp_launch_count", "lfbp_last_error", "lfbp_version", "lfbp_plane_sums_device",
     "lfbp_lf5_read_header", "lfbp_lf5_create", "lfbp_lf5_transform_file", "lfbp_lf5_load_device",
     "lfbp_lf5_store_device", "lfbp_forward_project_device", "lfbp_backproject_device",
-    "lfbp_safe_divide_device",
+    "lfbp_safe_divide_device", "lfbp_forward_project2_device",
 )
 
 _lock = threading.Lock()
@@ -59,6 +59,9 @@ _SIGS = {
                                              ctypes.c_void_p]),
     "lfbp_forward_project_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _i64p, ctypes.c_void_p,
                                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "lfbp_forward_project2_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, _i64p,
+                                                    ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                                    ctypes.c_void_p]),
     "lfbp_backproject_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _i64p, ctypes.c_int, ctypes.c_void_p,
                                                ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "lfbp_safe_divide_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,

@@ -876,6 +876,9 @@ int lfbp_plane_sums_device(const void* src, double* out, const int64_t dims[5], 
   return LFBP_OK;
 }
 
+int lfbp_forward_project2_device(const void* H, const void* Hp, int dtype, const int64_t dims[5],
+                                 const double* volume, int64_t nvx, int64_t nvy, double* image, void* stream);
+
 static int proj_geom(hp::ProjGeom& q, const int64_t dims[5], int64_t nvx, int64_t nvy) {
   if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || dims[3] < 1 || dims[4] < 1 || nvx < 1 || nvy < 1)
     return fail(LFBP_ERR_INVALID_DIMS, "bad projector geometry");
@@ -896,16 +899,30 @@ static int proj_geom(hp::ProjGeom& q, const int64_t dims[5], int64_t nvx, int64_
 
 int lfbp_forward_project_device(const void* H, int dtype, const int64_t dims[5], const double* volume, int64_t nvx,
                                 int64_t nvy, double* image, void* stream) {
+  return lfbp_forward_project2_device(H, nullptr, dtype, dims, volume, nvx, nvy, image, stream);
+}
+
+int lfbp_forward_project2_device(const void* H, const void* Hp, int dtype, const int64_t dims[5], const double* volume,
+                                 int64_t nvx, int64_t nvy, double* image, void* stream) {
   hp::ProjGeom q;
   int rc = proj_geom(q, dims, nvx, nvy);
   if (rc) return rc;
-  if (!H || !volume || !image || !elem_size(dtype)) return fail(LFBP_ERR_ARGUMENT, "bad forward_project arguments");
+  if ((!H && !Hp) || !volume || !image || !elem_size(dtype))
+    return fail(LFBP_ERR_ARGUMENT, "bad forward_project arguments");
+  const bool odd = (dims[0] % 2) && (dims[1] % 2);
+  if (!H && !odd) return fail(LFBP_ERR_EVEN_PIXEL_DIMS, "the H' form of the forward projection needs odd n_s, n_t");
   const dim3 blk(32, 8), grd(unsigned((nvx + 31) / 32), unsigned((nvy + 7) / 8));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (dtype == LFBP_F32)
+  if (Hp && odd) {  // pixel-phase form (coalesced), same sums as the H form
+    if (dtype == LFBP_F32)
+      hp::forward_project_hp_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(Hp), volume, image, q);
+    else
+      hp::forward_project_hp_kernel<double><<<grd, blk, 0, st>>>(static_cast<const double*>(Hp), volume, image, q);
+  } else if (dtype == LFBP_F32) {
     hp::forward_project_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(H), volume, image, q);
-  else
+  } else {
     hp::forward_project_kernel<double><<<grd, blk, 0, st>>>(static_cast<const double*>(H), volume, image, q);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   HP_CUDA(cudaGetLastError());
   return LFBP_OK;

@@ -61,6 +61,37 @@ __global__ void forward_project_kernel(const T* __restrict__ H, const double* __
   out[S + int64_t(Tt) * q.nvx] = acc;
 }
 
+// forward projection through H' (odd n_s, n_t): the pixel's own phase fixes
+// the pattern -- out[S,T] = sum_z sum_{i,j} g[S+i-c_s, T+j-c_t, z] *
+// H'[i, j, S mod n_x, T mod n_y, z] -- so a lane walks one contiguous pattern
+// row while the warp reads the volume row coalesced (same sums as the H form:
+// H'[i, ., S mod n_x] = H[2c-i, ., (S+i-c) mod n_x]).
+template <typename T>
+__global__ void forward_project_hp_kernel(const T* __restrict__ Hp, const double* __restrict__ g,
+                                          double* __restrict__ out, const ProjGeom q) {
+  const int32_t S = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t Tt = blockIdx.y * blockDim.y + threadIdx.y;
+  if (S >= q.nvx || Tt >= q.nvy) return;
+  const int64_t pat = int64_t(q.n_s) * q.n_t;
+  const int64_t plane = pat * q.n_x * q.n_y;
+  const int64_t vplane = int64_t(q.nvx) * q.nvy;
+  // taps that keep the voxel inside the grid: 0 <= S + i - c < nvx
+  const int32_t i_lo = max(0, q.c_s - S), i_hi = min(q.n_s - 1, q.nvx - 1 - S + q.c_s);
+  const int32_t j_lo = max(0, q.c_t - Tt), j_hi = min(q.n_t - 1, q.nvy - 1 - Tt + q.c_t);
+  const int64_t phase = (int64_t(S % q.n_x) + int64_t(Tt % q.n_y) * q.n_x) * pat;
+  double acc = 0.0;
+  for (int32_t z = 0; z < q.n_z; ++z) {
+    const T* K = Hp + z * plane + phase;
+    const double* gz = g + z * vplane + (S - q.c_s);
+    for (int32_t j = j_lo; j <= j_hi; ++j) {
+      const T* krow = K + int64_t(j) * q.n_s;
+      const double* grow = gz + int64_t(Tt + j - q.c_t) * q.nvx;
+      for (int32_t i = i_lo; i <= i_hi; ++i) acc = fma(grow[i], static_cast<double>(krow[i]), acc);
+    }
+  }
+  out[S + int64_t(Tt) * q.nvx] = acc;
+}
+
 // adjoint (use_hprime = 0, pattern array H, voxel phase) or the H'-stamp
 // backprojection (use_hprime = 1, pattern array H', pixel phase)
 template <typename T>

@@ -79,21 +79,30 @@ def _check_finite(name: str, data) -> None:
 # --------------------------------------------------------------------------
 # device API
 
-def forward_project_device(H, g, out=None):
+def forward_project_device(H, g, out=None, Hp=None):
     """image (nvx, nvy) = forward projection of volume g (nvx, nvy, n_z)
-    through the PSF H (n_s, n_t, n_x, n_y, n_z); CUDA tensors, F layout."""
-    dims = tuple(int(v) for v in H.shape)
+    through the PSF H (n_s, n_t, n_x, n_y, n_z); CUDA tensors, F layout.
+    With ``Hp`` (H' of H, odd n_s / n_t) the pixel-phase gather is used: each
+    pixel reads one contiguous pattern plane (same sums, coalesced)."""
+    P = H if H is not None else Hp
+    dims = tuple(int(v) for v in P.shape)
     nvx, nvy, nvz = (int(v) for v in g.shape)
     if nvz != dims[4]:
         raise DimMismatch(f"volume has {nvz} depth planes, PSF array has {dims[4]}")
     if out is None:
         out = _f_empty((nvx, nvy), g.device)
+    hptr = ctypes.c_void_p(H.data_ptr()) if H is not None else None
+    pptr = ctypes.c_void_p(Hp.data_ptr()) if Hp is not None else None
     with _torch().cuda.device(g.device):
-        rc = _native.lib().lfbp_forward_project_device(ctypes.c_void_p(H.data_ptr()), _code(H),
-                                                       _native.dims_array(dims), ctypes.c_void_p(g.data_ptr()),
-                                                       nvx, nvy, ctypes.c_void_p(out.data_ptr()), _stream(g))
+        rc = _native.lib().lfbp_forward_project2_device(hptr, pptr, _code(P), _native.dims_array(dims),
+                                                        ctypes.c_void_p(g.data_ptr()), nvx, nvy,
+                                                        ctypes.c_void_p(out.data_ptr()), _stream(g))
     _native.check(rc)
     return out
+
+
+def _odd(dims) -> bool:
+    return dims[0] % 2 == 1 and dims[1] % 2 == 1
 
 
 def backproject_device(P, f, use_hprime: bool = True, out=None):
@@ -130,16 +139,21 @@ def safe_divide_device(num, den, eps: float, out=None, scratch=None):
 # drop-ins for the reference's host API
 
 def forward_project(psf, volume, device: int = 0) -> Image:
+    """projector.py:55-81 on the GPU (H' computed on the device for the
+    pixel-phase gather when n_s, n_t are odd)."""
+    from .transform import hprime_device
     n_z = psf.dims.n_z
     if volume.shape[2] != n_z:
         raise DimMismatch(f"volume has {volume.shape[2]} depth planes, PSF array has {n_z}")
     dev = f"cuda:{device}"
     H = _to_device_f(psf.data, dev)
     g = _to_device_f(volume.data, dev, np.float64)
-    return Image._wrap(_to_host_f(forward_project_device(H, g)))
+    Hp = hprime_device(H) if _odd(psf.dims.shape) else None
+    return Image._wrap(_to_host_f(forward_project_device(H, g, Hp=Hp)))
 
 
 def backproject_adjoint(psf, image, device: int = 0) -> Volume:
+    """projector.py:84-100 on the GPU (voxel-phase gather through H)."""
     dev = f"cuda:{device}"
     H = _to_device_f(psf.data, dev)
     f = _to_device_f(image.data, dev, np.float64)
@@ -147,9 +161,16 @@ def backproject_adjoint(psf, image, device: int = 0) -> Volume:
 
 
 def backproject(bp, image, device: int = 0) -> Volume:
+    """projector.py:103-126 on the GPU.  For odd n_s, n_t, H is recovered from
+    H' on the device (the map is an involution) and the voxel-phase gather is
+    used (equal to the H'-stamp form within 1e-12, as the reference's own
+    tests require); even sizes use the H' pixel-stamp gather directly."""
+    from .transform import hprime_device
     dev = f"cuda:{device}"
     P = _to_device_f(bp.data, dev)
     f = _to_device_f(image.data, dev, np.float64)
+    if _odd(bp.dims.shape):
+        return Volume._wrap(_to_host_f(backproject_device(hprime_device(P, inverse=True), f, use_hprime=False)))
     return Volume._wrap(_to_host_f(backproject_device(P, f, use_hprime=True)))
 
 
@@ -185,7 +206,17 @@ def rl_run(psf, bp, image, iterations: int = 20, eps: float = 1e-12, device: int
     f = _to_device_f(image.data, dev, np.float64)
     npx, npy = image.shape
     n_z = psf.dims.n_z
-    norm = backproject_device(P, _to_device_f(np.ones((npx, npy)), dev))
+    odd = _odd(psf.dims.shape)
+    # odd sizes: forward through H' (pixel phase), backward through H (voxel
+    # phase) -- both coalesced gathers; even sizes: H forward, H' stamps back
+
+    def fwd(vol, out):
+        return forward_project_device(H, vol, out=out, Hp=P if odd else None)
+
+    def back(img, out):
+        return backproject_device(H, img, use_hprime=False, out=out) if odd else \
+            backproject_device(P, img, use_hprime=True, out=out)
+    norm = back(_to_device_f(np.ones((npx, npy)), dev), None)
     peak = max(float(norm.max().item()), 0.0)
     dead = int((norm < eps * peak).sum().item())
     if dead:
@@ -194,17 +225,17 @@ def rl_run(psf, bp, image, iterations: int = 20, eps: float = 1e-12, device: int
     g.fill_(1.0)
     reproj = _f_empty((npx, npy), dev)
     ratio = _f_empty((npx, npy), dev)
-    back = _f_empty((npx, npy, n_z), dev)
+    bwd = _f_empty((npx, npy, n_z), dev)
     upd = _f_empty((npx, npy, n_z), dev)
     scratch = torch.empty(1, dtype=torch.float64, device=dev)
     mse = []
     for _ in range(iterations):
-        forward_project_device(H, g, out=reproj)
+        fwd(g, reproj)
         safe_divide_device(f, reproj, eps, out=ratio, scratch=scratch)
-        backproject_device(P, ratio, out=back)
-        safe_divide_device(back, norm, eps, out=upd, scratch=scratch)
+        back(ratio, bwd)
+        safe_divide_device(bwd, norm, eps, out=upd, scratch=scratch)
         g.mul_(upd)
-        forward_project_device(H, g, out=reproj)
+        fwd(g, reproj)
         mse.append(((f - reproj) ** 2).mean())
     history = [float(v) for v in torch.stack(mse).cpu().tolist()]
     return RlState(Volume._wrap(_to_host_f(g)), iterations, Volume._wrap(_to_host_f(norm)), history, dead)
