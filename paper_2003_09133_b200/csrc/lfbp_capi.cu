@@ -897,6 +897,37 @@ static int proj_geom(hp::ProjGeom& q, const int64_t dims[5], int64_t nvx, int64_
   return LFBP_OK;
 }
 
+// polyphase correlation (projector.cuh): pad+split the input planes, then one
+// block per (coarse tile, output phase[, output plane])
+static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const double* in, int32_t in_planes,
+                     double* out, bool forward, cudaStream_t st) {
+  hp::PolyGeom pg;
+  pg.kc = (q.nvx + q.n_x - 1) / q.n_x;
+  pg.lc = (q.nvy + q.n_y - 1) / q.n_y;
+  pg.hx = (q.n_s + q.n_x - 1) / q.n_x + 1;
+  pg.hy = (q.n_t + q.n_y - 1) / q.n_y + 3;
+  pg.kp = pg.kc + 2 * pg.hx;
+  pg.lp = pg.lc + 2 * pg.hy;
+  const int64_t n_sub = int64_t(pg.kp) * pg.lp * q.n_x * q.n_y * in_planes;
+  double* sub = nullptr;
+  HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sub), size_t(n_sub) * sizeof(double), st));
+  const int pb = int(std::min<int64_t>(4736, (n_sub + 255) / 256));
+  hp::polyphase_pad_kernel<<<pb, 256, 0, st>>>(in, sub, q, pg, in_planes);
+  const int32_t n_ph = q.n_x * q.n_y;
+  const dim3 blk(32, 4);
+  const dim3 grd(unsigned((pg.kc + 31) / 32), unsigned((pg.lc + 15) / 16),
+                 unsigned(forward ? n_ph : n_ph * q.n_z));
+  if (dtype == LFBP_F32)
+    hp::poly_corr_kernel<float><<<grd, blk, 0, st>>>(sub, static_cast<const float*>(K), out, q, pg, forward);
+  else
+    hp::poly_corr_kernel<double><<<grd, blk, 0, st>>>(sub, static_cast<const double*>(K), out, q, pg, forward);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(sub, st);
+  if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "projector: %s", cudaGetErrorString(e));
+  return LFBP_OK;
+}
+
 int lfbp_forward_project_device(const void* H, int dtype, const int64_t dims[5], const double* volume, int64_t nvx,
                                 int64_t nvy, double* image, void* stream) {
   return lfbp_forward_project2_device(H, nullptr, dtype, dims, volume, nvx, nvy, image, stream);
@@ -913,7 +944,8 @@ int lfbp_forward_project2_device(const void* H, const void* Hp, int dtype, const
   if (!H && !odd) return fail(LFBP_ERR_EVEN_PIXEL_DIMS, "the H' form of the forward projection needs odd n_s, n_t");
   const dim3 blk(32, 8), grd(unsigned((nvx + 31) / 32), unsigned((nvy + 7) / 8));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (Hp && odd) {  // pixel-phase form (coalesced), same sums as the H form
+  if (Hp && odd) {  // pixel-phase form, same sums as the H form
+    if (env_int("LFBP_PROJ_SIMPLE", 0) == 0) return poly_corr(Hp, dtype, q, volume, q.n_z, image, true, st);
     if (dtype == LFBP_F32)
       hp::forward_project_hp_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(Hp), volume, image, q);
     else
@@ -936,6 +968,8 @@ int lfbp_backproject_device(const void* P, int dtype, const int64_t dims[5], int
   if (!P || !volume || !image || !elem_size(dtype)) return fail(LFBP_ERR_ARGUMENT, "bad backproject arguments");
   const dim3 blk(32, 8), grd(unsigned((npx + 31) / 32), unsigned((npy + 7) / 8), unsigned(dims[4]));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!use_hprime && env_int("LFBP_PROJ_SIMPLE", 0) == 0)  // adjoint: voxel-phase polyphase correlation
+    return poly_corr(P, dtype, q, image, 1, volume, false, st);
   if (dtype == LFBP_F32)
     hp::backproject_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(P), image, volume, q, use_hprime);
   else

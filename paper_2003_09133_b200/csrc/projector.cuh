@@ -131,6 +131,102 @@ __global__ void backproject_kernel(const T* __restrict__ P, const double* __rest
   out[X + int64_t(Y) * q.nvx + int64_t(z) * q.nvx * q.nvy] = acc;
 }
 
+// ---- polyphase form (odd and even sizes alike) ---------------------------
+// Both directions are "fixed output phase" correlations:
+//   out[P] = sum_{a,b} in[P + (a, b) - (C_s, C_t)] * K_phase(P)[a, b]
+// (forward: in = g[:, :, z] summed over z, K = H' when n_s, n_t are odd;
+// backward: in = f, K = H, one output plane per z).  Splitting the input into
+// its n_x * n_y phase sub-images (zero-padded by a halo, PolyGeom) makes every
+// tap read, for the 32 lanes of one output phase at consecutive coarse k,
+// 32 consecutive doubles of one sub-image (coalesced), while the pattern
+// value is one broadcast; each thread keeps 4 outputs along the coarse y axis
+// and slides a 4-row register window over the taps b = r' + n_y * n.
+struct PolyGeom {
+  int32_t kc, lc;   // coarse extent of the output grid: ceil(nvx / n_x), ceil(nvy / n_y)
+  int32_t hx, hy;   // halo (coarse cells) on each side
+  int32_t kp, lp;   // padded sub-image extent: kc + 2 hx, lc + 2 hy
+};
+
+// in (nvx, nvy, planes) F-order -> sub[plane][ry][rx][ll][kk] (kk fastest)
+__global__ void polyphase_pad_kernel(const double* __restrict__ in, double* __restrict__ sub, const ProjGeom q,
+                                     const PolyGeom pg, int32_t planes) {
+  const int64_t per = int64_t(pg.kp) * pg.lp;
+  const int64_t total = per * q.n_x * q.n_y * planes;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t kk = int32_t(i % pg.kp);
+    int64_t r = i / pg.kp;
+    const int32_t ll = int32_t(r % pg.lp);
+    r /= pg.lp;
+    const int32_t rx = int32_t(r % q.n_x);
+    r /= q.n_x;
+    const int32_t ry = int32_t(r % q.n_y);
+    const int64_t z = r / q.n_y;
+    const int32_t x = rx + q.n_x * (kk - pg.hx), y = ry + q.n_y * (ll - pg.hy);
+    sub[i] = (x >= 0 && x < q.nvx && y >= 0 && y < q.nvy) ? in[x + int64_t(y) * q.nvx + z * int64_t(q.nvx) * q.nvy]
+                                                           : 0.0;
+  }
+}
+
+__device__ __forceinline__ int32_t floordiv(int32_t a, int32_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// grid: x = coarse k tiles of 32, y = coarse l tiles of 4 * blockDim.y,
+//       z = phase (px + n_x * py) [+ n_x * n_y * zout for the backward pass]
+// forward (n_in_planes == n_z): out image, sum over z; backward (n_in_planes
+// == 1): out[:, :, zout]
+template <typename T>
+__global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict__ sub, const T* __restrict__ K,
+                                                        double* __restrict__ out, const ProjGeom q, const PolyGeom pg,
+                                                        int32_t forward) {
+  const int32_t n_ph = q.n_x * q.n_y;
+  const int32_t ph = blockIdx.z % n_ph;
+  const int32_t zout = forward ? 0 : blockIdx.z / n_ph;
+  const int32_t px = ph % q.n_x, py = ph / q.n_x;
+  const int32_t k = blockIdx.x * 32 + threadIdx.x;
+  const int32_t l0 = (blockIdx.y * blockDim.y + threadIdx.y) * 4;
+  if (k >= pg.kc || l0 >= pg.lc) return;
+  const int64_t pat = int64_t(q.n_s) * q.n_t;
+  const int64_t sub_plane = int64_t(pg.kp) * pg.lp;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int32_t z_lo = forward ? 0 : zout, z_hi = forward ? q.n_z : zout + 1;
+  for (int32_t z = z_lo; z < z_hi; ++z) {
+    const T* Kz = K + (int64_t(z) * n_ph + ph) * pat;
+    const double* subz = sub + (forward ? int64_t(z) * n_ph * sub_plane : 0);
+    for (int32_t r2 = 0; r2 < q.n_y && r2 < q.n_t; ++r2) {
+      const int32_t rho_y = py - q.c_t + r2;
+      const int32_t ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
+      const int32_t lyy = floordiv(rho_y, q.n_y) + pg.hy;
+      const int32_t n_taps = (q.n_t - r2 + q.n_y - 1) / q.n_y;   // b = r2 + n_y * n < n_t
+      for (int32_t a = 0; a < q.n_s; ++a) {
+        const int32_t rho_x = px - q.c_s + a;
+        const int32_t rxx = ((rho_x % q.n_x) + q.n_x) % q.n_x;
+        const int32_t kxx = floordiv(rho_x, q.n_x) + pg.hx;
+        const double* col = subz + (int64_t(ryy) * q.n_x + rxx) * sub_plane + (k + kxx) +
+                            int64_t(l0 + lyy) * pg.kp;
+        const T* kcol = Kz + a + int64_t(r2) * q.n_s;
+        double w0 = col[0], w1 = col[pg.kp], w2 = col[2 * pg.kp];
+        for (int32_t n = 0; n < n_taps; ++n) {
+          const double w3 = col[int64_t(n + 3) * pg.kp];
+          const double v = static_cast<double>(kcol[int64_t(n) * q.n_y * q.n_s]);
+          acc[0] = fma(w0, v, acc[0]);
+          acc[1] = fma(w1, v, acc[1]);
+          acc[2] = fma(w2, v, acc[2]);
+          acc[3] = fma(w3, v, acc[3]);
+          w0 = w1;
+          w1 = w2;
+          w2 = w3;
+        }
+      }
+    }
+  }
+  const int32_t X = px + q.n_x * k;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int32_t Y = py + q.n_y * (l0 + j);
+    if (X < q.nvx && Y < q.nvy && l0 + j < pg.lc)
+      out[X + int64_t(Y) * q.nvx + (forward ? 0 : int64_t(zout) * q.nvx * q.nvy)] = acc[j];
+  }
+}
+
 // _safe_divide (projector.py:135-145): num / den where den >= eps * max(den)
 // (and den > 0 when eps * max == 0), else 0; `peak` is max(den) on the device
 __global__ void safe_divide_kernel(const double* __restrict__ num, const double* __restrict__ den,
