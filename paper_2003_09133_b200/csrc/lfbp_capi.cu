@@ -914,16 +914,24 @@ static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const doub
   const int pb = int(std::min<int64_t>(4736, (n_sub + 255) / 256));
   hp::polyphase_pad_kernel<<<pb, 256, 0, st>>>(in, sub, q, pg, in_planes);
   const int32_t n_ph = q.n_x * q.n_y;
+  const int64_t img = int64_t(q.nvx) * q.nvy;
+  double* part = nullptr;  // forward: per-plane partial images
+  if (forward) HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), size_t(img * q.n_z) * sizeof(double), st));
   const dim3 blk(32, 4);
-  const dim3 grd(unsigned((pg.kc + 31) / 32), unsigned((pg.lc + 15) / 16),
-                 unsigned(forward ? n_ph : n_ph * q.n_z));
+  const dim3 grd(unsigned((pg.kc + 31) / 32), unsigned((pg.lc + 15) / 16), unsigned(n_ph * q.n_z));
+  double* dst = forward ? part : out;
   if (dtype == LFBP_F32)
-    hp::poly_corr_kernel<float><<<grd, blk, 0, st>>>(sub, static_cast<const float*>(K), out, q, pg, forward);
+    hp::poly_corr_kernel<float><<<grd, blk, 0, st>>>(sub, static_cast<const float*>(K), dst, q, pg, forward);
   else
-    hp::poly_corr_kernel<double><<<grd, blk, 0, st>>>(sub, static_cast<const double*>(K), out, q, pg, forward);
+    hp::poly_corr_kernel<double><<<grd, blk, 0, st>>>(sub, static_cast<const double*>(K), dst, q, pg, forward);
   g_launches.fetch_add(2, std::memory_order_relaxed);
+  if (forward) {
+    hp::sum_planes_kernel<<<int(std::min<int64_t>(1184, (img + 255) / 256)), 256, 0, st>>>(part, out, img, q.n_z);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(sub, st);
+  if (part) cudaFreeAsync(part, st);
   if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "projector: %s", cudaGetErrorString(e));
   return LFBP_OK;
 }

@@ -170,16 +170,16 @@ __global__ void polyphase_pad_kernel(const double* __restrict__ in, double* __re
 __device__ __forceinline__ int32_t floordiv(int32_t a, int32_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 // grid: x = coarse k tiles of 32, y = coarse l tiles of 4 * blockDim.y,
-//       z = phase (px + n_x * py) [+ n_x * n_y * zout for the backward pass]
-// forward (n_in_planes == n_z): out image, sum over z; backward (n_in_planes
-// == 1): out[:, :, zout]
+//       z = phase (px + n_x * py) + n_x * n_y * zout; out[:, :, zout] is the
+// backprojected plane (backward, input f shared by all z) or the partial
+// image of depth plane zout (forward, input g[:, :, zout]; summed afterwards)
 template <typename T>
 __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict__ sub, const T* __restrict__ K,
                                                         double* __restrict__ out, const ProjGeom q, const PolyGeom pg,
                                                         int32_t forward) {
   const int32_t n_ph = q.n_x * q.n_y;
   const int32_t ph = blockIdx.z % n_ph;
-  const int32_t zout = forward ? 0 : blockIdx.z / n_ph;
+  const int32_t zout = blockIdx.z / n_ph;  // forward: the depth plane this block sums (partial image per z)
   const int32_t px = ph % q.n_x, py = ph / q.n_x;
   const int32_t k = blockIdx.x * 32 + threadIdx.x;
   const int32_t l0 = (blockIdx.y * blockDim.y + threadIdx.y) * 4;
@@ -187,8 +187,7 @@ __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict
   const int64_t pat = int64_t(q.n_s) * q.n_t;
   const int64_t sub_plane = int64_t(pg.kp) * pg.lp;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const int32_t z_lo = forward ? 0 : zout, z_hi = forward ? q.n_z : zout + 1;
-  for (int32_t z = z_lo; z < z_hi; ++z) {
+  for (int32_t z = zout; z < zout + 1; ++z) {
     const T* Kz = K + (int64_t(z) * n_ph + ph) * pat;
     const double* subz = sub + (forward ? int64_t(z) * n_ph * sub_plane : 0);
     for (int32_t r2 = 0; r2 < q.n_y && r2 < q.n_t; ++r2) {
@@ -196,14 +195,21 @@ __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict
       const int32_t ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
       const int32_t lyy = floordiv(rho_y, q.n_y) + pg.hy;
       const int32_t n_taps = (q.n_t - r2 + q.n_y - 1) / q.n_y;   // b = r2 + n_y * n < n_t
+      // tap a walks the sub-images rx = (px - c_s + a) mod n_x, stepping the
+      // coarse offset when rx wraps (no division in the loop)
+      const int32_t rho0 = px - q.c_s;
+      int32_t rxx = ((rho0 % q.n_x) + q.n_x) % q.n_x;
+      int32_t kxx = floordiv(rho0, q.n_x) + pg.hx;
+      const double* row0 = subz + int64_t(ryy) * q.n_x * sub_plane + k + int64_t(l0 + lyy) * pg.kp;
       for (int32_t a = 0; a < q.n_s; ++a) {
-        const int32_t rho_x = px - q.c_s + a;
-        const int32_t rxx = ((rho_x % q.n_x) + q.n_x) % q.n_x;
-        const int32_t kxx = floordiv(rho_x, q.n_x) + pg.hx;
-        const double* col = subz + (int64_t(ryy) * q.n_x + rxx) * sub_plane + (k + kxx) +
-                            int64_t(l0 + lyy) * pg.kp;
+        const double* col = row0 + int64_t(rxx) * sub_plane + kxx;
         const T* kcol = Kz + a + int64_t(r2) * q.n_s;
+        if (++rxx == q.n_x) {
+          rxx = 0;
+          ++kxx;
+        }
         double w0 = col[0], w1 = col[pg.kp], w2 = col[2 * pg.kp];
+#pragma unroll 4
         for (int32_t n = 0; n < n_taps; ++n) {
           const double w3 = col[int64_t(n + 3) * pg.kp];
           const double v = static_cast<double>(kcol[int64_t(n) * q.n_y * q.n_s]);
@@ -222,8 +228,16 @@ __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int32_t Y = py + q.n_y * (l0 + j);
-    if (X < q.nvx && Y < q.nvy && l0 + j < pg.lc)
-      out[X + int64_t(Y) * q.nvx + (forward ? 0 : int64_t(zout) * q.nvx * q.nvy)] = acc[j];
+    if (X < q.nvx && Y < q.nvy && l0 + j < pg.lc) out[X + int64_t(Y) * q.nvx + int64_t(zout) * q.nvx * q.nvy] = acc[j];
+  }
+}
+
+// forward: image = sum over z of the per-plane partial images (fixed order)
+__global__ void sum_planes_kernel(const double* __restrict__ part, double* __restrict__ out, int64_t n, int32_t planes) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double a = 0.0;
+    for (int32_t z = 0; z < planes; ++z) a += part[i + z * n];
+    out[i] = a;
   }
 }
 
