@@ -111,6 +111,11 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
 
 
+def _dtype_tag(dtype) -> str:
+    """The element type the path moves: "f32" / "f64" (copied as 4 / 8-byte words)."""
+    return {4: "f32", 8: "f64"}[np.dtype(dtype).itemsize]
+
+
 def _dist():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -156,7 +161,7 @@ def run_reference(args, w):
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": np.dtype(w.dtype).name, "data": "synthetic (seeded BASELINE law)",
+        "dtype": _dtype_tag(w.dtype), "data": "synthetic (seeded BASELINE law)",
         "config": {"workload": f"{w.name} {w.shape} {np.dtype(w.dtype).name} seed {w.seed}",
                    "sample_planes": planes},
         "helems_per_s": round(H.size * args.steps / total, 1),
@@ -340,7 +345,7 @@ def main():
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
-            "dtype": np.dtype(w.dtype).name, "data": "synthetic (seeded BASELINE.json law, see synth.py)",
+            "dtype": _dtype_tag(w.dtype), "data": "synthetic (seeded BASELINE.json law, see synth.py)",
             "config": {"workload": f"{w.name} {w.shape} {np.dtype(w.dtype).name} seed {w.seed}",
                        "per_rank_shape": list(shape),
                        "parallelism": f"z-slab x{world}, no collective on the data path",
