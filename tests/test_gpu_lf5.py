@@ -104,3 +104,22 @@ def test_load_and_store_device_slabs(tmp_path):
     torch.cuda.synchronize()
     got = np.fromfile(fout, dtype=np.float32, offset=32)
     assert got.tobytes() == hprime_oracle(H).tobytes(order="F")
+
+
+def test_cli_transform_and_verify(tmp_path, capsys):
+    _torch()
+    from paper_2003_09133_b200 import lf5
+    from paper_2003_09133_b200.__main__ import main
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    H = random_psf_like_reference((21, 19, 7, 5, 3), density=0.8, seed=1, dtype=np.float32)
+    fin, fout = tmp_path / "in.lf5", tmp_path / "out.lf5"
+    lf5.save(H, fin)
+    assert main(["transform", str(fin), str(fout)]) == 0
+    assert main(["verify", str(fin), "--against", str(fout)]) == 0
+    assert "PASS" in capsys.readouterr().out
+    bad = np.fromfile(fout, dtype=np.uint8)
+    bad[32 + 4 * 100] ^= 1                      # element 100 (0-based, F order)
+    bad.tofile(fout)
+    assert main(["verify", str(fin), "--against", str(fout)]) == 1
+    out = capsys.readouterr().out
+    assert "FAIL" in out and "(s,t,x,y,z)=(17, 5, 1, 1, 1)" in out

@@ -275,7 +275,7 @@ def test_dropin_pageable_host_modes_multi_chunk(monkeypatch, mode):
     assert fbytes(bp.data) == fbytes(hprime_oracle(H, threads=7))
 
 
-def test_multi_host_staged_pageable_output():
+def test_multi_host_staged_pageable_output(monkeypatch):
     """lfbp_hprime_multi with pageable src and dst (staging both ways)."""
     _torch()
     import ctypes
@@ -286,12 +286,27 @@ def test_multi_host_staged_pageable_output():
     H = random_psf_like_reference(shape, density=1.0, seed=4, dtype=np.float32)
     out = np.empty_like(H, order="F")
     devs = (ctypes.c_int * 2)(0, 0)
-    import os
-    os.environ["LFBP_CHUNK_MB"] = "1"
-    try:
-        rc = _native.lib().lfbp_hprime_multi(H.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p),
-                                             _native.dims_array(shape), _native.F32, 0, 2, devs, _native.HOST_STAGE)
-    finally:
-        del os.environ["LFBP_CHUNK_MB"]
+    monkeypatch.setenv("LFBP_CHUNK_MB", "1")
+    rc = _native.lib().lfbp_hprime_multi(H.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p),
+                                         _native.dims_array(shape), _native.F32, 0, 2, devs, _native.HOST_STAGE)
     _native.check(rc)
     assert fbytes(out) == fbytes(hprime_oracle(H))
+
+
+def test_rank_slabs_gather_into_shared_host_array(tmp_path):
+    """Per-rank z-slabs transformed on the device and copied straight into one
+    shared host H' at their plane offsets (shard.device_slab_to_shared)."""
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device
+    from paper_2003_09133_b200.shard import device_slab_to_shared, open_shared_host, rank_slab
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    shape = (45, 41, 9, 7, 10)
+    H = random_psf_like_reference(shape, density=1.0, seed=12, dtype=np.float32)
+    shared = open_shared_host(str(tmp_path / "hp.f32"), shape, np.float32, create=True)
+    for rank in range(3):
+        slab_shape, z0, z1 = rank_slab(shape, 3, rank)
+        slab = to_device(np.asfortranarray(H[..., z0:z1]))
+        device_slab_to_shared(shared, z0, hprime_device(slab))
+    torch.cuda.synchronize()
+    shared.flush()
+    assert fbytes(np.asarray(shared)) == fbytes(hprime_oracle(H))

@@ -83,3 +83,11 @@ def test_create_sizes_the_file(tmp_path):
     _native.check(_native.lib().lfbp_lf5_create(bytes(p), _native.dims_array((5, 5, 3, 3, 4)), 1))
     assert p.stat().st_size == 32 + 5 * 5 * 3 * 3 * 4 * 4
     assert lf5.read_header(p) == ((5, 5, 3, 3, 4), np.dtype("<f4"))
+
+
+def test_cli_plan_and_errors(tmp_path, capsys):
+    from paper_2003_09133_b200.__main__ import main
+    assert main(["plan", "195,195,15,15,51"]) == 0
+    assert '"J"' in capsys.readouterr().out
+    assert main(["transform", str(tmp_path / "missing.lf5"), str(tmp_path / "o.lf5")]) == 2
+    assert "IoError" in capsys.readouterr().err
