@@ -310,3 +310,28 @@ def test_rank_slabs_gather_into_shared_host_array(tmp_path):
     torch.cuda.synchronize()
     shared.flush()
     assert fbytes(np.asarray(shared)) == fbytes(hprime_oracle(H))
+
+
+def test_cuda_graph_capture_and_replay():
+    """The device entry point is capture-safe (the autotuner skips a
+    capturing stream): a CUDA graph of K1 launches replays bit-exactly."""
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    shape = (55, 55, 11, 11, 9)
+    H = random_psf_like_reference(shape, density=1.0, seed=6, dtype=np.float32)
+    src = to_device(H)
+    out = torch.zeros_like(src)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        hprime_device(src, out=out, stream=s)      # warm (plan caches) outside capture
+    s.synchronize()
+    out.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        hprime_device(src, out=out, stream=s)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert to_host(out).tobytes() == fbytes(hprime_oracle(H))
