@@ -897,6 +897,8 @@ static int proj_geom(hp::ProjGeom& q, const int64_t dims[5], int64_t nvx, int64_
   return LFBP_OK;
 }
 
+constexpr int kPolyRL = 8;  // coarse rows per thread in poly_corr_kernel
+
 // polyphase correlation (projector.cuh): pad+split the input planes, then one
 // block per (coarse tile, output phase[, output plane])
 static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const double* in, int32_t in_planes,
@@ -905,7 +907,8 @@ static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const doub
   pg.kc = (q.nvx + q.n_x - 1) / q.n_x;
   pg.lc = (q.nvy + q.n_y - 1) / q.n_y;
   pg.hx = (q.n_s + q.n_x - 1) / q.n_x + 1;
-  pg.hy = (q.n_t + q.n_y - 1) / q.n_y + 3;
+  const int32_t N = (q.n_t + q.n_y - 1) / q.n_y;  // taps per residue class along y
+  pg.hy = N + kPolyRL - 1;
   pg.kp = pg.kc + 2 * pg.hx;
   pg.lp = pg.lc + 2 * pg.hy;
   const int64_t n_sub = int64_t(pg.kp) * pg.lp * q.n_x * q.n_y * in_planes;
@@ -918,12 +921,15 @@ static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const doub
   double* part = nullptr;  // forward: per-plane partial images
   if (forward) HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), size_t(img * q.n_z) * sizeof(double), st));
   const dim3 blk(32, 4);
-  const dim3 grd(unsigned((pg.kc + 31) / 32), unsigned((pg.lc + 15) / 16), unsigned(n_ph * q.n_z));
+  const dim3 grd(unsigned((pg.kc + 31) / 32), unsigned((pg.lc + 4 * kPolyRL - 1) / (4 * kPolyRL)),
+                 unsigned(n_ph * q.n_z));
   double* dst = forward ? part : out;
-  if (dtype == LFBP_F32)
-    hp::poly_corr_kernel<float><<<grd, blk, 0, st>>>(sub, static_cast<const float*>(K), dst, q, pg, forward);
-  else
-    hp::poly_corr_kernel<double><<<grd, blk, 0, st>>>(sub, static_cast<const double*>(K), dst, q, pg, forward);
+  if (dtype == LFBP_F32) {
+    hp::poly_corr_kernel<float, kPolyRL><<<grd, blk, 0, st>>>(sub, static_cast<const float*>(K), dst, q, pg, forward);
+  } else {
+    hp::poly_corr_kernel<double, kPolyRL><<<grd, blk, 0, st>>>(sub, static_cast<const double*>(K), dst, q, pg,
+                                                                forward);
+  }
   g_launches.fetch_add(2, std::memory_order_relaxed);
   if (forward) {
     hp::sum_planes_kernel<<<int(std::min<int64_t>(1184, (img + 255) / 256)), 256, 0, st>>>(part, out, img, q.n_z);

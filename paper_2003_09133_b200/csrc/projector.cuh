@@ -173,7 +173,7 @@ __device__ __forceinline__ int32_t floordiv(int32_t a, int32_t b) { return a >= 
 //       z = phase (px + n_x * py) + n_x * n_y * zout; out[:, :, zout] is the
 // backprojected plane (backward, input f shared by all z) or the partial
 // image of depth plane zout (forward, input g[:, :, zout]; summed afterwards)
-template <typename T>
+template <typename T, int RL>
 __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict__ sub, const T* __restrict__ K,
                                                         double* __restrict__ out, const ProjGeom q, const PolyGeom pg,
                                                         int32_t forward) {
@@ -182,51 +182,64 @@ __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict
   const int32_t zout = blockIdx.z / n_ph;  // forward: the depth plane this block sums (partial image per z)
   const int32_t px = ph % q.n_x, py = ph / q.n_x;
   const int32_t k = blockIdx.x * 32 + threadIdx.x;
-  const int32_t l0 = (blockIdx.y * blockDim.y + threadIdx.y) * 4;
+  const int32_t l0 = (blockIdx.y * blockDim.y + threadIdx.y) * RL;
   if (k >= pg.kc || l0 >= pg.lc) return;
   const int64_t pat = int64_t(q.n_s) * q.n_t;
   const int64_t sub_plane = int64_t(pg.kp) * pg.lp;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int32_t z = zout; z < zout + 1; ++z) {
-    const T* Kz = K + (int64_t(z) * n_ph + ph) * pat;
-    const double* subz = sub + (forward ? int64_t(z) * n_ph * sub_plane : 0);
-    for (int32_t r2 = 0; r2 < q.n_y && r2 < q.n_t; ++r2) {
-      const int32_t rho_y = py - q.c_t + r2;
-      const int32_t ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
-      const int32_t lyy = floordiv(rho_y, q.n_y) + pg.hy;
-      const int32_t n_taps = (q.n_t - r2 + q.n_y - 1) / q.n_y;   // b = r2 + n_y * n < n_t
-      // tap a walks the sub-images rx = (px - c_s + a) mod n_x, stepping the
-      // coarse offset when rx wraps (no division in the loop)
-      const int32_t rho0 = px - q.c_s;
-      int32_t rxx = ((rho0 % q.n_x) + q.n_x) % q.n_x;
-      int32_t kxx = floordiv(rho0, q.n_x) + pg.hx;
-      const double* row0 = subz + int64_t(ryy) * q.n_x * sub_plane + k + int64_t(l0 + lyy) * pg.kp;
-      for (int32_t a = 0; a < q.n_s; ++a) {
-        const double* col = row0 + int64_t(rxx) * sub_plane + kxx;
-        const T* kcol = Kz + a + int64_t(r2) * q.n_s;
-        if (++rxx == q.n_x) {
-          rxx = 0;
-          ++kxx;
+  double acc[RL];
+#pragma unroll
+  for (int j = 0; j < RL; ++j) acc[j] = 0.0;
+  const T* Kz = K + (int64_t(zout) * n_ph + ph) * pat;
+  const double* subz = sub + (forward ? int64_t(zout) * n_ph * sub_plane : 0);
+  const int64_t kstep = int64_t(q.n_y) * q.n_s;
+  for (int32_t r2 = 0; r2 < q.n_y && r2 < q.n_t; ++r2) {
+    const int32_t rho_y = py - q.c_t + r2;
+    const int32_t ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
+    const int32_t lyy = floordiv(rho_y, q.n_y) + pg.hy;
+    const int32_t n_taps = (q.n_t - r2 + q.n_y - 1) / q.n_y;   // b = r2 + n_y * n < n_t
+    // tap a walks the sub-images rx = (px - c_s + a) mod n_x, stepping the
+    // coarse offset when rx wraps (no division in the loop)
+    const int32_t rho0 = px - q.c_s;
+    int32_t rxx = ((rho0 % q.n_x) + q.n_x) % q.n_x;
+    int32_t kxx = floordiv(rho0, q.n_x) + pg.hx;
+    const double* row0 = subz + int64_t(ryy) * q.n_x * sub_plane + k + int64_t(l0 + lyy) * pg.kp;
+    const T* krow = Kz + int64_t(r2) * q.n_s;
+    for (int32_t a = 0; a < q.n_s; ++a) {
+      const double* col = row0 + int64_t(rxx) * sub_plane + kxx;
+      const T* kcol = krow + a;
+      if (++rxx == q.n_x) {
+        rxx = 0;
+        ++kxx;
+      }
+      // register window over RL consecutive coarse rows, slid one row per
+      // tap: blocks of RL taps use it as a circular buffer with static slot
+      // indices (no moves), the remaining taps shift it
+      double w[RL];
+#pragma unroll
+      for (int j = 0; j < RL - 1; ++j) w[j] = col[int64_t(j) * pg.kp];
+      int32_t n = 0;
+      for (; n + RL <= n_taps; n += RL) {
+#pragma unroll
+        for (int t = 0; t < RL; ++t) {
+          w[(RL - 1 + t) % RL] = col[int64_t(n + t + RL - 1) * pg.kp];
+          const double v = static_cast<double>(kcol[int64_t(n + t) * kstep]);
+#pragma unroll
+          for (int j = 0; j < RL; ++j) acc[j] = fma(w[(j + t) % RL], v, acc[j]);
         }
-        double w0 = col[0], w1 = col[pg.kp], w2 = col[2 * pg.kp];
-#pragma unroll 4
-        for (int32_t n = 0; n < n_taps; ++n) {
-          const double w3 = col[int64_t(n + 3) * pg.kp];
-          const double v = static_cast<double>(kcol[int64_t(n) * q.n_y * q.n_s]);
-          acc[0] = fma(w0, v, acc[0]);
-          acc[1] = fma(w1, v, acc[1]);
-          acc[2] = fma(w2, v, acc[2]);
-          acc[3] = fma(w3, v, acc[3]);
-          w0 = w1;
-          w1 = w2;
-          w2 = w3;
-        }
+      }
+      for (; n < n_taps; ++n) {
+        w[RL - 1] = col[int64_t(n + RL - 1) * pg.kp];
+        const double v = static_cast<double>(kcol[int64_t(n) * kstep]);
+#pragma unroll
+        for (int j = 0; j < RL; ++j) acc[j] = fma(w[j], v, acc[j]);
+#pragma unroll
+        for (int j = 0; j < RL - 1; ++j) w[j] = w[j + 1];
       }
     }
   }
   const int32_t X = px + q.n_x * k;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < RL; ++j) {
     const int32_t Y = py + q.n_y * (l0 + j);
     if (X < q.nvx && Y < q.nvy && l0 + j < pg.lc) out[X + int64_t(Y) * q.nvx + int64_t(zout) * q.nvx * q.nvy] = acc[j];
   }
