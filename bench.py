@@ -175,6 +175,15 @@ def run_reference(args, w):
     return 0
 
 
+def _max_over_ranks(x: float, world: int, device) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _verify_against_golden(out, w, shape):
     from paper_2003_09133_b200.verify import plane_digests
     path = os.path.join(ROOT, "tests", "golden", f"digests_{w.name}.json")
@@ -220,10 +229,17 @@ def main():
     from paper_2003_09133_b200.synth import baseline_psf
 
     rank, world, local = _dist()
+    # one process per GPU; LFBP_BENCH_BACKEND=gloo (+ device = local % count)
+    # only exercises the multi-rank plumbing on a box with fewer GPUs
+    backend = os.environ.get("LFBP_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     # this rank's slab
     if args.strong:
@@ -243,8 +259,9 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
+        torch.cuda.synchronize(dev)
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier(device_ids=[local]) if backend == "nccl" else dist.barrier()
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
@@ -275,10 +292,7 @@ def main():
     launches = _native.launch_count() - l0
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     elapsed_ms = sum(kern_ms) if flush is not None else t0.elapsed_time(t1)
-    tt = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    max_ms = float(tt.item())
+    max_ms = _max_over_ranks(elapsed_ms, world, dev if backend == "nccl" else "cpu")
 
     verified = None
     if not args.no_verify and rank == 0:
@@ -304,10 +318,7 @@ def main():
             host_call()
         barrier()
         e2e_s = time.perf_counter() - t
-        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_s = float(te.item())
+        e2e_s = _max_over_ranks(e2e_s, world, dev if backend == "nccl" else "cpu")
         ok = hashlib.sha256(host_out.numpy().tobytes()).hexdigest() == hashlib.sha256(
             out.permute(4, 3, 2, 1, 0).contiguous().view(-1).cpu().numpy().tobytes()).hexdigest()
         e2e = {"value": round(world * step_bytes * args.e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
@@ -366,7 +377,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        dist.barrier(device_ids=[local]) if backend == "nccl" else dist.barrier()
         dist.destroy_process_group()
     return 0
 
