@@ -920,9 +920,10 @@ static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const doub
   const int64_t img = int64_t(q.nvx) * q.nvy;
   double* part = nullptr;  // forward: per-plane partial images
   if (forward) HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), size_t(img * q.n_z) * sizeof(double), st));
-  const dim3 blk(32, 4);
-  const dim3 grd(unsigned((pg.kc + 31) / 32), unsigned((pg.lc + 4 * kPolyRL - 1) / (4 * kPolyRL)),
-                 unsigned(n_ph * q.n_z));
+  const dim3 blk(128);
+  const dim3 grd(unsigned((int64_t(q.n_x) * pg.kc + 127) / 128), unsigned((pg.lc + kPolyRL - 1) / kPolyRL),
+                 unsigned(q.n_y * q.n_z));
+  (void)n_ph;
   double* dst = forward ? part : out;
   if (dtype == LFBP_F32) {
     hp::poly_corr_kernel<float, kPolyRL><<<grd, blk, 0, st>>>(sub, static_cast<const float*>(K), dst, q, pg, forward);

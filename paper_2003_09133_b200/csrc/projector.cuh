@@ -169,21 +169,24 @@ __global__ void polyphase_pad_kernel(const double* __restrict__ in, double* __re
 
 __device__ __forceinline__ int32_t floordiv(int32_t a, int32_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-// grid: x = coarse k tiles of 32, y = coarse l tiles of 4 * blockDim.y,
-//       z = phase (px + n_x * py) + n_x * n_y * zout; out[:, :, zout] is the
-// backprojected plane (backward, input f shared by all z) or the partial
-// image of depth plane zout (forward, input g[:, :, zout]; summed afterwards)
+// grid: x = (px, k) pairs / blockDim.x, y = coarse l tiles of RL rows,
+//       z = py + n_y * zout; out[:, :, zout] is the backprojected plane
+// (backward, input f shared by all z) or the partial image of depth plane
+// zout (forward, input g[:, :, zout]; summed afterwards)
 template <typename T, int RL>
 __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict__ sub, const T* __restrict__ K,
                                                         double* __restrict__ out, const ProjGeom q, const PolyGeom pg,
                                                         int32_t forward) {
   const int32_t n_ph = q.n_x * q.n_y;
-  const int32_t ph = blockIdx.z % n_ph;
-  const int32_t zout = blockIdx.z / n_ph;  // forward: the depth plane this block sums (partial image per z)
-  const int32_t px = ph % q.n_x, py = ph / q.n_x;
-  const int32_t k = blockIdx.x * 32 + threadIdx.x;
-  const int32_t l0 = (blockIdx.y * blockDim.y + threadIdx.y) * RL;
-  if (k >= pg.kc || l0 >= pg.lc) return;
+  // threads run over (px, k) with k fastest: a warp covers consecutive coarse
+  // cells of at most a few x-phases, so no lanes idle when kc < 32
+  const int32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t px = e / pg.kc, k = e - px * pg.kc;
+  const int32_t py = blockIdx.z % q.n_y;
+  const int32_t zout = blockIdx.z / q.n_y;  // forward: the depth plane this block sums (partial image per z)
+  const int32_t ph = px + q.n_x * py;
+  const int32_t l0 = blockIdx.y * RL;
+  if (px >= q.n_x || l0 >= pg.lc) return;
   const int64_t pat = int64_t(q.n_s) * q.n_t;
   const int64_t sub_plane = int64_t(pg.kp) * pg.lp;
   double acc[RL];
