@@ -26,7 +26,7 @@ import struct
 import numpy as np
 
 from . import _native
-from .arrays import BackprojArray, Dims5, PsfArray
+from .arrays import Dims5, PsfArray
 from .errors import DimsError, FormatError, InvalidDims, IoError
 
 log = logging.getLogger(__name__)

@@ -34,7 +34,7 @@ import os
 import numpy as np
 
 from . import _native
-from .arrays import BackprojArray, Dims5, PsfArray
+from .arrays import BackprojArray, PsfArray
 from .errors import EvenPixelDims, InvalidDims
 
 log = logging.getLogger(__name__)

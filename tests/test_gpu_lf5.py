@@ -2,7 +2,6 @@
 reference's `lfbp transform` path writes (tests/golden), at full C2 size
 against the reference's H' digest, plus z-slab device loads / stores."""
 import hashlib
-import os
 
 import numpy as np
 import pytest

@@ -5,7 +5,6 @@ arrays (tests/golden/small_cases.npz), against the reference's per-plane
 SHA-256 digests for the BASELINE configs (tests/golden/digests_C*.json), and
 against the CPU oracle (oracle/hprime_oracle.py) on seeded inputs.
 """
-import hashlib
 import os
 
 import numpy as np

@@ -32,7 +32,7 @@ def rel(a, b):
 
 
 def _arrays(H):
-    from paper_2003_09133_b200 import BackprojArray, Dims5, PsfArray, compute_backprojection
+    from paper_2003_09133_b200 import Dims5, PsfArray, compute_backprojection
     psf = PsfArray._wrap(Dims5.unchecked(*H.shape), H)
     return psf, compute_backprojection(psf)
 
