@@ -897,7 +897,34 @@ static int proj_geom(hp::ProjGeom& q, const int64_t dims[5], int64_t nvx, int64_
   return LFBP_OK;
 }
 
-constexpr int kPolyRL = 8;  // coarse rows per thread in poly_corr_kernel
+constexpr int kPolyRLMax = 16;  // max coarse rows per thread in poly_corr_kernel
+
+// rows per thread: the tap count N when 4 <= N <= 16 (whole taps blocks, no
+// register shifting), else 8
+inline int poly_rows(int32_t N) { return (N >= 4 && N <= kPolyRLMax) ? N : 8; }
+
+extern "C++" {
+template <typename T, int RL>
+void poly_launch_rl(dim3 grd, cudaStream_t st, const double* sub, const void* K, double* dst, const hp::ProjGeom& q,
+                    const hp::PolyGeom& pg, bool forward) {
+  hp::poly_corr_kernel<T, RL><<<grd, 128, 0, st>>>(sub, static_cast<const T*>(K), dst, q, pg, forward);
+}
+
+template <typename T>
+void poly_launch(int rl, dim3 grd, cudaStream_t st, const double* sub, const void* K, double* dst,
+                 const hp::ProjGeom& q, const hp::PolyGeom& pg, bool forward) {
+  switch (rl) {
+#define HP_RL(n) \
+  case n:        \
+    return poly_launch_rl<T, n>(grd, st, sub, K, dst, q, pg, forward);
+    HP_RL(4) HP_RL(5) HP_RL(6) HP_RL(7) HP_RL(9) HP_RL(10) HP_RL(11) HP_RL(12) HP_RL(13) HP_RL(14) HP_RL(15)
+    HP_RL(16)
+#undef HP_RL
+    default:
+      return poly_launch_rl<T, 8>(grd, st, sub, K, dst, q, pg, forward);
+  }
+}
+}  // extern "C++"
 
 // polyphase correlation (projector.cuh): pad+split the input planes, then one
 // block per (coarse tile, output phase[, output plane])
@@ -908,7 +935,8 @@ static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const doub
   pg.lc = (q.nvy + q.n_y - 1) / q.n_y;
   pg.hx = (q.n_s + q.n_x - 1) / q.n_x + 1;
   const int32_t N = (q.n_t + q.n_y - 1) / q.n_y;  // taps per residue class along y
-  pg.hy = N + kPolyRL - 1;
+  const int rl = poly_rows(N);
+  pg.hy = N + rl - 1;
   pg.kp = pg.kc + 2 * pg.hx;
   pg.lp = pg.lc + 2 * pg.hy;
   const int64_t n_sub = int64_t(pg.kp) * pg.lp * q.n_x * q.n_y * in_planes;
@@ -920,17 +948,14 @@ static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const doub
   const int64_t img = int64_t(q.nvx) * q.nvy;
   double* part = nullptr;  // forward: per-plane partial images
   if (forward) HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), size_t(img * q.n_z) * sizeof(double), st));
-  const dim3 blk(128);
-  const dim3 grd(unsigned((int64_t(q.n_x) * pg.kc + 127) / 128), unsigned((pg.lc + kPolyRL - 1) / kPolyRL),
+  const dim3 grd(unsigned((int64_t(q.n_x) * pg.kc + 127) / 128), unsigned((pg.lc + rl - 1) / rl),
                  unsigned(q.n_y * q.n_z));
   (void)n_ph;
   double* dst = forward ? part : out;
-  if (dtype == LFBP_F32) {
-    hp::poly_corr_kernel<float, kPolyRL><<<grd, blk, 0, st>>>(sub, static_cast<const float*>(K), dst, q, pg, forward);
-  } else {
-    hp::poly_corr_kernel<double, kPolyRL><<<grd, blk, 0, st>>>(sub, static_cast<const double*>(K), dst, q, pg,
-                                                                forward);
-  }
+  if (dtype == LFBP_F32)
+    poly_launch<float>(rl, grd, st, sub, K, dst, q, pg, forward);
+  else
+    poly_launch<double>(rl, grd, st, sub, K, dst, q, pg, forward);
   g_launches.fetch_add(2, std::memory_order_relaxed);
   if (forward) {
     hp::sum_planes_kernel<<<int(std::min<int64_t>(1184, (img + 255) / 256)), 256, 0, st>>>(part, out, img, q.n_z);
