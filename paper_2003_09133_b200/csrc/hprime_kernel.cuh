@@ -98,10 +98,19 @@ struct Unit {
 
 __device__ __forceinline__ Unit decode_unit(const HpPlan& p, uint32_t u) {
   Unit w;
-  uint32_t r = hp_div(p.ny_div, u);
-  w.y = u - r * p.ny_div.d;
-  uint32_t r2 = hp_div(p.nb_div, r);
-  const int32_t band = static_cast<int32_t>(r - r2 * p.nb_div.d);
+  int32_t band;
+  uint32_t r2;
+  if (p.flags & HP_FLAG_BAND_FASTEST) {  // consecutive units read adjacent t-bands
+    const uint32_t r = hp_div(p.nb_div, u);
+    band = static_cast<int32_t>(u - r * p.nb_div.d);
+    r2 = hp_div(p.ny_div, r);
+    w.y = r - r2 * p.ny_div.d;
+  } else {  // consecutive units: neighbouring y (their output rows interleave in L2)
+    const uint32_t r = hp_div(p.ny_div, u);
+    w.y = u - r * p.ny_div.d;
+    r2 = hp_div(p.nb_div, r);
+    band = static_cast<int32_t>(r - r2 * p.nb_div.d);
+  }
   uint32_t r3 = hp_div(p.nc_div, r2);
   const int32_t chunk = static_cast<int32_t>(r2 - r3 * p.nc_div.d);
   w.z = p.z_begin + r3;

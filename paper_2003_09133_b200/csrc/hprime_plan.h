@@ -64,6 +64,7 @@ HP_HD uint32_t hp_mod(const HpFastDiv& f, uint32_t n) {
 }
 
 #define HP_FLAG_LOAD_EVICT_FIRST 1  // L2 evict_first hint on the bulk loads of H
+#define HP_FLAG_BAND_FASTEST 4      // unit order: t-band fastest instead of y
 
 struct HpPlan {
   // geometry of the (chunk) arrays the kernel sees

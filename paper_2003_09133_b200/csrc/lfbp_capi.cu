@@ -1,9 +1,13 @@
 // C-ABI of the B200-native H -> H' rearrangement (see include/lfbp_hprime.h).
 //
 // Host runtime around the K1 kernel: dims validation with the reference's
-// rules, the launch planner (work-unit shape, smem ring, persistent grid),
-// device-array entry point, a chunked H2D / kernel / D2H pipeline for host
-// arrays, the z-slab multi-GPU launcher, and the K2 device comparator.
+// rules, the launch planner (work-unit shape, smem ring, persistent grid) and
+// its autotuner, the device-array entry point and the z-slab multi-GPU
+// launcher.  One translation unit; the rest is included:
+//   host_pipeline.inc   chunked H2D / K1 / D2H pipeline for host arrays
+//   verify_capi.inc     K2 comparator, K3 plane sums
+//   projector_capi.inc  K5 projector launchers
+//   lf5_stream.inc      LF5 file streaming (K4 value check)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -333,309 +337,7 @@ int check_common(const int64_t dims[5], int dtype, int inverse) {
 
 int64_t plane_elems(const int64_t d[5]) { return d[0] * d[1] * d[2] * d[3]; }
 
-// ---- host thread pool: parallel memcpy / pread / pwrite of staging chunks ----
-class HostPool {
- public:
-  explicit HostPool(int n) {
-    for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { run(i); });
-  }
-  ~HostPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& t : th_) t.join();
-  }
-  // fn(a, b) over [0, n) split into one part per worker (parts aligned to
-  // `align` bytes); returns when every part is done
-  void for_range(size_t n, size_t align, const std::function<void(size_t, size_t)>& fn) {
-    if (th_.empty() || n < (size_t(4) << 20)) {
-      fn(0, n);
-      return;
-    }
-    std::lock_guard<std::mutex> one_job(call_mu_);  // callers from several device threads take turns
-    std::unique_lock<std::mutex> lk(mu_);
-    fn_ = &fn;
-    n_ = n;
-    align_ = align;
-    pending_ = int(th_.size());
-    ++gen_;
-    cv_.notify_all();
-    done_.wait(lk, [this] { return pending_ == 0; });
-  }
-  void copy(void* dst, const void* src, size_t n) {
-    uint8_t* d = static_cast<uint8_t*>(dst);
-    const uint8_t* s = static_cast<const uint8_t*>(src);
-    for_range(n, 64, [&](size_t a, size_t b) { memcpy(d + a, s + a, b - a); });
-  }
-
- private:
-  void run(int i) {
-    uint64_t seen = 0;
-    for (;;) {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-      if (stop_) return;
-      seen = gen_;
-      const size_t parts = th_.size();
-      const size_t chunk = ((n_ / parts) + align_ - 1) / align_ * align_;
-      const size_t a = std::min(n_, chunk * i), b = std::min(n_, a + chunk);
-      const std::function<void(size_t, size_t)>* fn = fn_;
-      lk.unlock();
-      if (b > a) (*fn)(a, b);
-      lk.lock();
-      if (--pending_ == 0) done_.notify_one();
-    }
-  }
-  std::vector<std::thread> th_;
-  std::mutex call_mu_;
-  std::mutex mu_;
-  std::condition_variable cv_, done_;
-  const std::function<void(size_t, size_t)>* fn_ = nullptr;
-  size_t n_ = 0, align_ = 64;
-  int pending_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
-};
-
-HostPool& copy_pool() {
-  static HostPool pool(std::max(1, std::min(16, env_int("LFBP_COPY_THREADS",
-                                                        int(std::thread::hardware_concurrency()) / 2))));
-  return pool;
-}
-
-// ---- host pipeline workspace (one per device, reused across calls) ----
-constexpr int kPipe = 3;
-
-struct Workspace {
-  std::mutex mu;
-  int dev = -1;
-  size_t cap = 0;
-  void* in[kPipe] = {};
-  void* out[kPipe] = {};
-  cudaStream_t s_h2d = nullptr, s_cmp = nullptr, s_d2h = nullptr;
-  cudaEvent_t h2d_done[kPipe] = {}, cmp_done[kPipe] = {}, d2h_done[kPipe] = {};
-  bool init = false;
-  size_t stage_cap = 0;             // pinned staging for pageable host arrays
-  void* pin_in[kPipe] = {};
-  void* pin_out[kPipe] = {};
-};
-
-std::mutex g_ws_mu;
-std::map<int, std::unique_ptr<Workspace>> g_ws;
-
-Workspace& workspace(int dev) {
-  std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto& w = g_ws[dev];
-  if (!w) {
-    w.reset(new Workspace());
-    w->dev = dev;
-  }
-  return *w;
-}
-
-int ws_reserve(Workspace& w, size_t bytes) {
-  if (!w.init) {
-    HP_CUDA(cudaStreamCreateWithFlags(&w.s_h2d, cudaStreamNonBlocking));
-    HP_CUDA(cudaStreamCreateWithFlags(&w.s_cmp, cudaStreamNonBlocking));
-    HP_CUDA(cudaStreamCreateWithFlags(&w.s_d2h, cudaStreamNonBlocking));
-    for (int k = 0; k < kPipe; ++k) {
-      HP_CUDA(cudaEventCreateWithFlags(&w.h2d_done[k], cudaEventDisableTiming));
-      HP_CUDA(cudaEventCreateWithFlags(&w.cmp_done[k], cudaEventDisableTiming));
-      HP_CUDA(cudaEventCreateWithFlags(&w.d2h_done[k], cudaEventDisableTiming));
-    }
-    w.init = true;
-  }
-  if (bytes <= w.cap) return LFBP_OK;
-  for (int k = 0; k < kPipe; ++k) {
-    if (w.in[k]) cudaFree(w.in[k]);
-    if (w.out[k]) cudaFree(w.out[k]);
-    w.in[k] = w.out[k] = nullptr;
-  }
-  w.cap = 0;
-  for (int k = 0; k < kPipe; ++k) {
-    HP_CUDA(cudaMalloc(&w.in[k], bytes));
-    HP_CUDA(cudaMalloc(&w.out[k], bytes));
-  }
-  w.cap = bytes;
-  return LFBP_OK;
-}
-
-int ws_reserve_staging(Workspace& w, size_t bytes) {
-  if (bytes <= w.stage_cap) return LFBP_OK;
-  for (int k = 0; k < kPipe; ++k) {
-    if (w.pin_in[k]) cudaFreeHost(w.pin_in[k]);
-    if (w.pin_out[k]) cudaFreeHost(w.pin_out[k]);
-    w.pin_in[k] = w.pin_out[k] = nullptr;
-  }
-  w.stage_cap = 0;
-  for (int k = 0; k < kPipe; ++k) {
-    HP_CUDA(cudaHostAlloc(&w.pin_in[k], bytes, cudaHostAllocPortable));
-    HP_CUDA(cudaHostAlloc(&w.pin_out[k], bytes, cudaHostAllocPortable));
-  }
-  w.stage_cap = bytes;
-  return LFBP_OK;
-}
-
-bool is_pinned(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-
-struct HostPin {
-  void* ptr = nullptr;
-  bool registered = false;
-  ~HostPin() {
-    if (registered) cudaHostUnregister(ptr);
-  }
-};
-
-int maybe_pin(HostPin& pin, const void* p, size_t bytes, int flags) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    a.type = cudaMemoryTypeUnregistered;
-  }
-  if (a.type != cudaMemoryTypeUnregistered || !(flags & LFBP_HOST_REGISTER)) return LFBP_OK;
-  cudaError_t e = cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterPortable);
-  if (e == cudaErrorHostMemoryAlreadyRegistered) {
-    cudaGetLastError();
-    return LFBP_OK;
-  }
-  if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
-  pin.ptr = const_cast<void*>(p);
-  pin.registered = true;
-  return LFBP_OK;
-}
-
-// Optional hooks of the host pipeline: where a chunk's input comes from and
-// where its output goes when it is not a host array (the LF5 file path).
-// Offsets are byte offsets of the chunk in the whole array.
-using FillFn = std::function<int(uint8_t* pinned, int64_t off, size_t bytes)>;
-using FlushFn = std::function<int(const uint8_t* pinned, int64_t off, size_t bytes)>;
-
-// K4: elements failing `v >= 0` (negative or NaN), the reference's PsfArray
-// value check (arrays.py:106-107), counted on the device
-template <typename T>
-__global__ void count_invalid_kernel(const T* __restrict__ a, int64_t n, unsigned long long* count) {
-  unsigned long long c = 0;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    c += !(a[i] >= T(0));
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
-}
-
-// planes [z0, z1) of host src -> host dst through device `dev`; with `fill`
-// / `flush` the chunks are produced / consumed by the hooks instead; with
-// `invalid` (device counter) the input values are checked like PsfArray's
-int host_slab(const uint8_t* src, uint8_t* dst, const int64_t dims[5], int E, int dev, int64_t z0, int64_t z1,
-              int flags, const FillFn* fill = nullptr, const FlushFn* flush = nullptr,
-              unsigned long long* invalid = nullptr) {
-  HP_CUDA(cudaSetDevice(dev));
-  const int64_t pb = plane_elems(dims) * E;
-  const int64_t nz = z1 - z0;
-  if (nz <= 0) return LFBP_OK;
-  const int64_t target = int64_t(env_int("LFBP_CHUNK_MB", 64)) << 20;
-  const int64_t cp = std::max<int64_t>(1, std::min<int64_t>(nz, target / std::max<int64_t>(pb, 1)));
-  const int64_t n_chunks = (nz + cp - 1) / cp;
-  // pageable arrays: stage through pinned buffers (parallel host memcpy
-  // overlapped with the DMA), or pin them in place, or let the driver stage
-  const bool stage_in = fill || ((flags & LFBP_HOST_STAGE) && !is_pinned(src + z0 * pb));
-  const bool stage_out = flush || ((flags & LFBP_HOST_STAGE) && !is_pinned(dst + z0 * pb));
-  const int reg_flags = flags & LFBP_HOST_REGISTER;
-  HostPin pin_in, pin_out;
-  int rc = stage_in ? LFBP_OK : maybe_pin(pin_in, src + z0 * pb, size_t(nz * pb), reg_flags);
-  if (rc) return rc;
-  rc = stage_out ? LFBP_OK : maybe_pin(pin_out, dst + z0 * pb, size_t(nz * pb), reg_flags);
-  if (rc) return rc;
-  Workspace& w = workspace(dev);
-  std::lock_guard<std::mutex> lk(w.mu);
-  rc = ws_reserve(w, size_t(cp * pb));
-  if (rc) return rc;
-  if (stage_in || stage_out) {
-    rc = ws_reserve_staging(w, size_t(cp * pb));
-    if (rc) return rc;
-  }
-  auto chunk_range = [&](int64_t c, int64_t& a, size_t& bytes) {
-    a = z0 + c * cp;
-    bytes = size_t(std::min<int64_t>(cp, z1 - a) * pb);
-  };
-  auto drain = [&](int64_t c) -> int {  // staged output of chunk c -> dst / flush hook
-    int64_t a;
-    size_t bytes;
-    chunk_range(c, a, bytes);
-    const int k = int(c % kPipe);
-    HP_CUDA(cudaEventSynchronize(w.d2h_done[k]));
-    if (flush) return (*flush)(static_cast<const uint8_t*>(w.pin_out[k]), a * pb, bytes);
-    copy_pool().copy(dst + a * pb, w.pin_out[k], bytes);
-    return LFBP_OK;
-  };
-  for (int64_t c = 0; c < n_chunks; ++c) {
-    const int k = int(c % kPipe);
-    int64_t a;
-    size_t bytes;
-    chunk_range(c, a, bytes);
-    const int64_t planes = int64_t(bytes) / pb;
-    const uint8_t* h_src = src ? src + a * pb : nullptr;
-    if (stage_in) {
-      if (c >= kPipe) HP_CUDA(cudaEventSynchronize(w.h2d_done[k]));  // pin_in[k] free
-      if (fill) {
-        rc = (*fill)(static_cast<uint8_t*>(w.pin_in[k]), a * pb, bytes);
-        if (rc) return rc;
-      } else {
-        copy_pool().copy(w.pin_in[k], h_src, bytes);
-      }
-      h_src = static_cast<const uint8_t*>(w.pin_in[k]);
-    }
-    if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_h2d, w.cmp_done[k], 0));  // in[k] consumed
-    HP_CUDA(cudaMemcpyAsync(w.in[k], h_src, bytes, cudaMemcpyHostToDevice, w.s_h2d));
-    HP_CUDA(cudaEventRecord(w.h2d_done[k], w.s_h2d));
-    HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.h2d_done[k], 0));
-    if (c >= kPipe) HP_CUDA(cudaStreamWaitEvent(w.s_cmp, w.d2h_done[k], 0));  // out[k] drained
-    if (invalid) {
-      const int64_t n = int64_t(bytes) / E;
-      const int blocks = int(std::min<int64_t>(1184, (n + 255) / 256));
-      if (E == 4)
-        count_invalid_kernel<float><<<blocks, 256, 0, w.s_cmp>>>(static_cast<const float*>(w.in[k]), n, invalid);
-      else
-        count_invalid_kernel<double><<<blocks, 256, 0, w.s_cmp>>>(static_cast<const double*>(w.in[k]), n, invalid);
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      HP_CUDA(cudaGetLastError());
-    }
-    int64_t cd[5] = {dims[0], dims[1], dims[2], dims[3], planes};
-    Knobs kn;
-    if (!env_knobs_set()) tuned_knobs(TuneKey{dims[0], dims[1], dims[2], dims[3], E, dev}, kn);
-    HpPlan p;
-    rc = make_plan(p, cd, E, 0, planes, int64_t(bytes), dev, kn);
-    if (rc) return rc;
-    rc = launch(p, w.in[k], w.out[k], w.s_cmp);
-    if (rc) return rc;
-    HP_CUDA(cudaEventRecord(w.cmp_done[k], w.s_cmp));
-    HP_CUDA(cudaStreamWaitEvent(w.s_d2h, w.cmp_done[k], 0));
-    HP_CUDA(cudaMemcpyAsync(stage_out ? static_cast<uint8_t*>(w.pin_out[k]) : dst + a * pb, w.out[k], bytes,
-                            cudaMemcpyDeviceToHost, w.s_d2h));
-    HP_CUDA(cudaEventRecord(w.d2h_done[k], w.s_d2h));
-    // chunk c - (kPipe - 1) frees its pinned output before pin_out is reused
-    if (stage_out && c >= kPipe - 1) {
-      rc = drain(c - (kPipe - 1));
-      if (rc) return rc;
-    }
-  }
-  if (stage_out)
-    for (int64_t c = std::max<int64_t>(0, n_chunks - (kPipe - 1)); c < n_chunks; ++c) {
-      rc = drain(c);
-      if (rc) return rc;
-    }
-  HP_CUDA(cudaStreamSynchronize(w.s_d2h));
-  HP_CUDA(cudaStreamSynchronize(w.s_cmp));
-  HP_CUDA(cudaStreamSynchronize(w.s_h2d));
-  return LFBP_OK;
-}
+#include "host_pipeline.inc"
 
 // ---- K2: device bitwise comparator ----
 __global__ void compare_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int64_t n,
@@ -778,36 +480,6 @@ int lfbp_hprime_multi(const void* src, void* dst, const int64_t dims[5], int dty
   return LFBP_OK;
 }
 
-int lfbp_compare_device(const void* a, const void* b, int64_t nbytes, int64_t* n_diff, int64_t* first_diff,
-                        void* stream) {
-  if (!a || !b || nbytes < 0 || !n_diff || !first_diff) return fail(LFBP_ERR_ARGUMENT, "bad compare arguments");
-  if ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15)
-    return fail(LFBP_ERR_ARGUMENT, "compare buffers must be 16-byte aligned");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  unsigned long long* scratch = nullptr;
-  HP_CUDA(cudaMalloc(&scratch, 2 * sizeof(unsigned long long)));
-  unsigned long long init[2] = {0ull, ~0ull};
-  cudaError_t e = cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const DevProps dp = device_props(dev);
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(int64_t(dp.sm_count) * 8, (nbytes / 16 + 255) / 256));
-    compare_kernel<<<int(blocks), 256, 0, st>>>(static_cast<const uint8_t*>(a), static_cast<const uint8_t*>(b),
-                                                nbytes, scratch, scratch + 1);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    e = cudaGetLastError();
-  }
-  unsigned long long res[2] = {0ull, ~0ull};
-  if (e == cudaSuccess) e = cudaMemcpyAsync(res, scratch, sizeof(res), cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  cudaFree(scratch);
-  if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "compare: %s", cudaGetErrorString(e));
-  *n_diff = int64_t(res[0]);
-  *first_diff = res[0] ? int64_t(res[1]) : -1;
-  return LFBP_OK;
-}
-
 int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len) {
   int rc = check_common(dims, dtype, 0);
   if (rc) return rc;
@@ -839,199 +511,9 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
   return LFBP_OK;
 }
 
-int lfbp_plane_sums_device(const void* src, double* out, const int64_t dims[5], int dtype, int64_t z_begin,
-                           int64_t z_end, void* stream) {
-  // any positive shape (the reference sums unchecked-dims arrays too, fileio.py:95-104)
-  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || dims[3] < 1 || dims[4] < 1)
-    return fail(LFBP_ERR_INVALID_DIMS, "dims must all be >= 1");
-  if (!elem_size(dtype)) return fail(LFBP_ERR_ARGUMENT, "dtype code %d is not 1 (f32) or 2 (f64)", dtype);
-  if (!src || !out) return fail(LFBP_ERR_ARGUMENT, "null device pointer");
-  if (z_begin < 0 || z_end > dims[4] || z_begin > z_end)
-    return fail(LFBP_ERR_ARGUMENT, "plane range [%lld, %lld) outside [0, %lld)", (long long)z_begin,
-                (long long)z_end, (long long)dims[4]);
-  const int64_t K = dims[2] * dims[3];
-  if (K > 8192) return fail(LFBP_ERR_UNSUPPORTED, "slice of %lld values exceeds the sort limit 8192", (long long)K);
-  int P = 32;
-  while (P < K) P <<= 1;
-  const int64_t n_slices = dims[0] * dims[1] * (z_end - z_begin);
-  if (n_slices == 0) return LFBP_OK;
-  int dev = 0;
-  HP_CUDA(cudaGetDevice(&dev));
-  const DevProps dp = device_props(dev);
-  const int wpc = int(std::max<int64_t>(1, std::min<int64_t>(8, (dp.smem_optin / 2) / (int64_t(P) * 8))));
-  const size_t smem = size_t(wpc) * P * 8;
-  const int64_t blocks = std::min<int64_t>((n_slices + wpc - 1) / wpc, int64_t(dp.sm_count) * 16);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (dtype == LFBP_F32) {
-    HP_CUDA(cudaFuncSetAttribute(hp::plane_sums_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    hp::plane_sums_kernel<float><<<int(blocks), 32 * wpc, smem, st>>>(
-        static_cast<const float*>(src), out, int32_t(dims[0]), int32_t(dims[1]), int32_t(K), P, z_begin, n_slices);
-  } else {
-    HP_CUDA(cudaFuncSetAttribute(hp::plane_sums_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    hp::plane_sums_kernel<double><<<int(blocks), 32 * wpc, smem, st>>>(
-        static_cast<const double*>(src), out, int32_t(dims[0]), int32_t(dims[1]), int32_t(K), P, z_begin, n_slices);
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  HP_CUDA(cudaGetLastError());
-  return LFBP_OK;
-}
+#include "verify_capi.inc"
 
-int lfbp_forward_project2_device(const void* H, const void* Hp, int dtype, const int64_t dims[5],
-                                 const double* volume, int64_t nvx, int64_t nvy, double* image, void* stream);
-
-static int proj_geom(hp::ProjGeom& q, const int64_t dims[5], int64_t nvx, int64_t nvy) {
-  if (!dims || dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || dims[3] < 1 || dims[4] < 1 || nvx < 1 || nvy < 1)
-    return fail(LFBP_ERR_INVALID_DIMS, "bad projector geometry");
-  if (dims[0] * dims[1] * dims[2] * dims[3] >= (int64_t(1) << 31) || nvx * nvy >= (int64_t(1) << 31))
-    return fail(LFBP_ERR_UNSUPPORTED, "projector plane too large");
-  q.n_s = int32_t(dims[0]);
-  q.n_t = int32_t(dims[1]);
-  q.n_x = int32_t(dims[2]);
-  q.n_y = int32_t(dims[3]);
-  q.n_z = int32_t(dims[4]);
-  // pattern_centre (projector.py:26-32) minus one
-  q.c_s = int32_t(dims[0] % 2 ? (dims[0] + 1) / 2 - 1 : dims[0] / 2);
-  q.c_t = int32_t(dims[1] % 2 ? (dims[1] + 1) / 2 - 1 : dims[1] / 2);
-  q.nvx = int32_t(nvx);
-  q.nvy = int32_t(nvy);
-  return LFBP_OK;
-}
-
-constexpr int kPolyRLMax = 16;  // max coarse rows per thread in poly_corr_kernel
-
-// rows per thread: the tap count N when 4 <= N <= 16 (whole taps blocks, no
-// register shifting), else 8
-inline int poly_rows(int32_t N) { return (N >= 4 && N <= kPolyRLMax) ? N : 8; }
-
-extern "C++" {
-template <typename T, int RL>
-void poly_launch_rl(dim3 grd, cudaStream_t st, const double* sub, const void* K, double* dst, const hp::ProjGeom& q,
-                    const hp::PolyGeom& pg, bool forward) {
-  hp::poly_corr_kernel<T, RL><<<grd, 128, 0, st>>>(sub, static_cast<const T*>(K), dst, q, pg, forward);
-}
-
-template <typename T>
-void poly_launch(int rl, dim3 grd, cudaStream_t st, const double* sub, const void* K, double* dst,
-                 const hp::ProjGeom& q, const hp::PolyGeom& pg, bool forward) {
-  switch (rl) {
-#define HP_RL(n) \
-  case n:        \
-    return poly_launch_rl<T, n>(grd, st, sub, K, dst, q, pg, forward);
-    HP_RL(4) HP_RL(5) HP_RL(6) HP_RL(7) HP_RL(9) HP_RL(10) HP_RL(11) HP_RL(12) HP_RL(13) HP_RL(14) HP_RL(15)
-    HP_RL(16)
-#undef HP_RL
-    default:
-      return poly_launch_rl<T, 8>(grd, st, sub, K, dst, q, pg, forward);
-  }
-}
-}  // extern "C++"
-
-// polyphase correlation (projector.cuh): pad+split the input planes, then one
-// block per (coarse tile, output phase[, output plane])
-static int poly_corr(const void* K, int dtype, const hp::ProjGeom& q, const double* in, int32_t in_planes,
-                     double* out, bool forward, cudaStream_t st) {
-  hp::PolyGeom pg;
-  pg.kc = (q.nvx + q.n_x - 1) / q.n_x;
-  pg.lc = (q.nvy + q.n_y - 1) / q.n_y;
-  pg.hx = (q.n_s + q.n_x - 1) / q.n_x + 1;
-  const int32_t N = (q.n_t + q.n_y - 1) / q.n_y;  // taps per residue class along y
-  const int rl = poly_rows(N);
-  pg.hy = N + rl - 1;
-  pg.kp = pg.kc + 2 * pg.hx;
-  pg.lp = pg.lc + 2 * pg.hy;
-  const int64_t n_sub = int64_t(pg.kp) * pg.lp * q.n_x * q.n_y * in_planes;
-  double* sub = nullptr;
-  HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&sub), size_t(n_sub) * sizeof(double), st));
-  const int pb = int(std::min<int64_t>(4736, (n_sub + 255) / 256));
-  hp::polyphase_pad_kernel<<<pb, 256, 0, st>>>(in, sub, q, pg, in_planes);
-  const int32_t n_ph = q.n_x * q.n_y;
-  const int64_t img = int64_t(q.nvx) * q.nvy;
-  double* part = nullptr;  // forward: per-plane partial images
-  if (forward) HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), size_t(img * q.n_z) * sizeof(double), st));
-  const dim3 grd(unsigned((int64_t(q.n_x) * pg.kc + 127) / 128), unsigned((pg.lc + rl - 1) / rl),
-                 unsigned(q.n_y * q.n_z));
-  (void)n_ph;
-  double* dst = forward ? part : out;
-  if (dtype == LFBP_F32)
-    poly_launch<float>(rl, grd, st, sub, K, dst, q, pg, forward);
-  else
-    poly_launch<double>(rl, grd, st, sub, K, dst, q, pg, forward);
-  g_launches.fetch_add(2, std::memory_order_relaxed);
-  if (forward) {
-    hp::sum_planes_kernel<<<int(std::min<int64_t>(1184, (img + 255) / 256)), 256, 0, st>>>(part, out, img, q.n_z);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-  }
-  cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(sub, st);
-  if (part) cudaFreeAsync(part, st);
-  if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "projector: %s", cudaGetErrorString(e));
-  return LFBP_OK;
-}
-
-int lfbp_forward_project_device(const void* H, int dtype, const int64_t dims[5], const double* volume, int64_t nvx,
-                                int64_t nvy, double* image, void* stream) {
-  return lfbp_forward_project2_device(H, nullptr, dtype, dims, volume, nvx, nvy, image, stream);
-}
-
-int lfbp_forward_project2_device(const void* H, const void* Hp, int dtype, const int64_t dims[5], const double* volume,
-                                 int64_t nvx, int64_t nvy, double* image, void* stream) {
-  hp::ProjGeom q;
-  int rc = proj_geom(q, dims, nvx, nvy);
-  if (rc) return rc;
-  if ((!H && !Hp) || !volume || !image || !elem_size(dtype))
-    return fail(LFBP_ERR_ARGUMENT, "bad forward_project arguments");
-  const bool odd = (dims[0] % 2) && (dims[1] % 2);
-  if (!H && !odd) return fail(LFBP_ERR_EVEN_PIXEL_DIMS, "the H' form of the forward projection needs odd n_s, n_t");
-  const dim3 blk(32, 8), grd(unsigned((nvx + 31) / 32), unsigned((nvy + 7) / 8));
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (Hp && odd) {  // pixel-phase form, same sums as the H form
-    if (env_int("LFBP_PROJ_SIMPLE", 0) == 0) return poly_corr(Hp, dtype, q, volume, q.n_z, image, true, st);
-    if (dtype == LFBP_F32)
-      hp::forward_project_hp_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(Hp), volume, image, q);
-    else
-      hp::forward_project_hp_kernel<double><<<grd, blk, 0, st>>>(static_cast<const double*>(Hp), volume, image, q);
-  } else if (dtype == LFBP_F32) {
-    hp::forward_project_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(H), volume, image, q);
-  } else {
-    hp::forward_project_kernel<double><<<grd, blk, 0, st>>>(static_cast<const double*>(H), volume, image, q);
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  HP_CUDA(cudaGetLastError());
-  return LFBP_OK;
-}
-
-int lfbp_backproject_device(const void* P, int dtype, const int64_t dims[5], int use_hprime, const double* image,
-                            int64_t npx, int64_t npy, double* volume, void* stream) {
-  hp::ProjGeom q;
-  int rc = proj_geom(q, dims, npx, npy);
-  if (rc) return rc;
-  if (!P || !volume || !image || !elem_size(dtype)) return fail(LFBP_ERR_ARGUMENT, "bad backproject arguments");
-  const dim3 blk(32, 8), grd(unsigned((npx + 31) / 32), unsigned((npy + 7) / 8), unsigned(dims[4]));
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (!use_hprime && env_int("LFBP_PROJ_SIMPLE", 0) == 0)  // adjoint: voxel-phase polyphase correlation
-    return poly_corr(P, dtype, q, image, 1, volume, false, st);
-  if (dtype == LFBP_F32)
-    hp::backproject_kernel<float><<<grd, blk, 0, st>>>(static_cast<const float*>(P), image, volume, q, use_hprime);
-  else
-    hp::backproject_kernel<double><<<grd, blk, 0, st>>>(static_cast<const double*>(P), image, volume, q, use_hprime);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  HP_CUDA(cudaGetLastError());
-  return LFBP_OK;
-}
-
-int lfbp_safe_divide_device(const double* num, const double* den, double* out, int64_t n, double eps,
-                            double* scratch, void* stream) {
-  if (!num || !den || !out || !scratch || n < 0) return fail(LFBP_ERR_ARGUMENT, "bad safe_divide arguments");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  HP_CUDA(cudaMemsetAsync(scratch, 0, sizeof(double), st));
-  if (n == 0) return LFBP_OK;
-  const int blocks = int(std::min<int64_t>(1184, (n + 255) / 256));
-  hp::max_kernel<<<blocks, 256, 0, st>>>(den, n, scratch);
-  hp::safe_divide_kernel<<<blocks, 256, 0, st>>>(num, den, out, n, eps, scratch);
-  g_launches.fetch_add(2, std::memory_order_relaxed);
-  HP_CUDA(cudaGetLastError());
-  return LFBP_OK;
-}
+#include "projector_capi.inc"
 
 int64_t lfbp_launch_count(void) { return g_launches.load(); }
 
