@@ -123,7 +123,7 @@ bool env_knobs_set() {
 // neighbours; every one is bit-exact, they differ only in speed).
 const Knobs kCandidates[] = {
     {3, 48, 8, 8},  {4, 48, 12, 16}, {4, 48, 8, 8},  {4, 48, 8, 16},
-    {4, 32, 8, 16}, {3, 64, 8, 32},  {4, 48, 16, 16}, {4, 32, 4, 8},
+    {2, 96, 8, 16}, {3, 64, 8, 32},  {4, 48, 16, 16}, {2, 96, 8, 8},
 };
 
 // Work-unit shape, smem ring and persistent grid for one launch.
