@@ -26,7 +26,8 @@
  *   lfbp_lf5_*             -> read_lf5 / save / load_psf (fileio.py:46-113)
  *                             and the `lfbp transform` CLI (cli.py:115-126)
  *   lfbp_forward_project_device / lfbp_backproject_device /
- *   lfbp_safe_divide_device -> forward_project / backproject(_adjoint) /
+ *   lfbp_safe_divide_device, lfbp_safe_divide_peak_device, lfbp_max_device,
+ *   lfbp_rl_update_device   -> forward_project / backproject(_adjoint) /
  *                             _safe_divide, projector.py:55-145 (the H'
  *                             consumer; rl_run composes them)
  * Error codes mirror the reference's exceptions (errors.py:12-13, 32-33).
@@ -158,6 +159,23 @@ int lfbp_backproject_device(const void* P, int dtype, const int64_t dims[5], int
  * double. */
 int lfbp_safe_divide_device(const double* num, const double* den, double* out, int64_t n, double eps,
                             double* scratch, void* stream);
+
+/* *peak = max(0, max(x[0..n))) on the device (the `den.max()` of
+ * `_safe_divide`, projector.py:138, for one rank's z-slab; ranks combine
+ * their peaks with an all-reduce MAX before dividing). */
+int lfbp_max_device(const double* x, int64_t n, double* peak, void* stream);
+
+/* `_safe_divide` (projector.py:135-145) against a caller-supplied device
+ * peak: out = num / den where den >= eps * (*peak) (and den > 0 if that is
+ * 0), else 0; all zeros when *peak <= 0. */
+int lfbp_safe_divide_peak_device(const double* num, const double* den, double* out, int64_t n, double eps,
+                                 const double* peak, void* stream);
+
+/* The Richardson-Lucy update `g = g * _safe_divide(back, norm, eps)`
+ * (projector.py:192) in place, fused: g[i] *= (ok ? back[i] / norm[i] : 0)
+ * with ok as in lfbp_safe_divide_peak_device. */
+int lfbp_rl_update_device(double* g, const double* back, const double* norm, int64_t n, double eps,
+                          const double* peak, void* stream);
 
 /* The launch plan the kernel would use, as a JSON object in `buf` (for
  * tests, tuning and DESIGN.md).  Uses the current device's properties, or

@@ -26,7 +26,8 @@ EXPORTS = (
     "lfbp_launch_count", "lfbp_last_error", "lfbp_version", "lfbp_plane_sums_device",
     "lfbp_lf5_read_header", "lfbp_lf5_create", "lfbp_lf5_transform_file", "lfbp_lf5_load_device",
     "lfbp_lf5_store_device", "lfbp_forward_project_device", "lfbp_backproject_device",
-    "lfbp_safe_divide_device", "lfbp_forward_project2_device",
+    "lfbp_safe_divide_device", "lfbp_forward_project2_device", "lfbp_max_device",
+    "lfbp_safe_divide_peak_device", "lfbp_rl_update_device",
 )
 
 _lock = threading.Lock()
@@ -66,6 +67,12 @@ _SIGS = {
                                                ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "lfbp_safe_divide_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                                ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
+    "lfbp_max_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "lfbp_safe_divide_peak_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                    ctypes.c_int64, ctypes.c_double, ctypes.c_void_p,
+                                                    ctypes.c_void_p]),
+    "lfbp_rl_update_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                             ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
     "lfbp_launch_count": (ctypes.c_int64, []),
     "lfbp_last_error": (ctypes.c_char_p, []),
     "lfbp_version": (ctypes.c_char_p, []),

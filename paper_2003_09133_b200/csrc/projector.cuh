@@ -275,6 +275,24 @@ __global__ void safe_divide_kernel(const double* __restrict__ num, const double*
   }
 }
 
+// g *= _safe_divide(back, norm, eps)[i] (projector.py:192), fused
+__global__ void rl_update_kernel(double* __restrict__ g, const double* __restrict__ back,
+                                 const double* __restrict__ norm, int64_t n, double eps,
+                                 const double* __restrict__ peak) {
+  const double pk = *peak;
+  const double thr = eps * pk;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    double r = 0.0;
+    if (pk > 0.0) {
+      const double d = norm[i];
+      bool ok = d >= thr;
+      if (thr == 0.0) ok = ok && d > 0.0;
+      if (ok) r = back[i] / d;
+    }
+    g[i] = g[i] * r;
+  }
+}
+
 __device__ __forceinline__ void atomic_max_double(double* a, double v) {
   // nonnegative doubles order like their bit patterns; NaN / negatives never win
   if (!(v > 0.0)) return;

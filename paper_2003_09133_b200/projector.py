@@ -189,36 +189,90 @@ class RlState:
     dead_voxels: int = 0
 
 
-def rl_run(psf, bp, image, iterations: int = 20, eps: float = 1e-12, device: int = 0) -> RlState:
-    """Richardson-Lucy deconvolution (projector.py:162-196) with all
-    projections and updates resident on the GPU."""
+class DeviceSlabOps:
+    """The projection kernels over one z-slab of H / H' resident on a CUDA
+    device (C-ABI, csrc/projector.cuh).  ``rl_loop`` only calls these
+    methods, so the sharded orchestration can be checked on CPU (gloo) with
+    the oracle substituted -- the product path always runs these kernels.
+
+    Odd n_s, n_t: forward through H' (pixel-phase gather), backward through
+    H (voxel-phase gather), both coalesced; even sizes: H forward, H' stamps
+    back."""
+
+    def __init__(self, H, P, odd: bool):
+        self.H, self.P, self.odd = H, P, odd
+
+    def forward(self, g, out):
+        return forward_project_device(self.H, g, out=out, Hp=self.P if self.odd else None)
+
+    def back(self, img, out):
+        if self.odd:
+            return backproject_device(self.H, img, use_hprime=False, out=out)
+        return backproject_device(self.P, img, use_hprime=True, out=out)
+
+    @staticmethod
+    def max(x, peak):
+        with _torch().cuda.device(x.device):
+            _native.check(_native.lib().lfbp_max_device(ctypes.c_void_p(x.data_ptr()), x.numel(),
+                                                        ctypes.c_void_p(peak.data_ptr()), _stream(x)))
+        return peak
+
+    @staticmethod
+    def divide(num, den, eps, peak, out):
+        with _torch().cuda.device(num.device):
+            _native.check(_native.lib().lfbp_safe_divide_peak_device(
+                ctypes.c_void_p(num.data_ptr()), ctypes.c_void_p(den.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                num.numel(), float(eps), ctypes.c_void_p(peak.data_ptr()), _stream(num)))
+        return out
+
+    @staticmethod
+    def update(g, back, norm, eps, peak):
+        with _torch().cuda.device(g.device):
+            _native.check(_native.lib().lfbp_rl_update_device(
+                ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(back.data_ptr()), ctypes.c_void_p(norm.data_ptr()),
+                g.numel(), float(eps), ctypes.c_void_p(peak.data_ptr()), _stream(g)))
+        return g
+
+
+def rl_loop(ops, f, n_z: int, iterations: int, eps: float, sharded: bool = False, group=None):
+    """Richardson-Lucy (projector.py:162-196) over this rank's n_z planes.
+
+    ``f`` is the measured image (float64, replicated on every rank).  With a
+    ``torch.distributed`` group (``sharded``) the volume is z-sharded: the forward
+    projection is a sum over planes, so each rank's partial image is summed
+    with one all-reduce (the only exchange; 8*npx*npy bytes), and the
+    normalizer's peak / dead-voxel count are reduced once.  Everything else
+    is per-plane and stays local.  ``sharded`` turns the reductions on;
+    ``group`` is the process group (None: the default group).
+
+    The reference projects the updated estimate twice per iteration (for
+    the residual, then again at the top of the next iteration); the second
+    is the same deterministic computation on the same estimate, so its
+    result is reused: one forward and one backward projection per
+    iteration.  Returns (estimate, normalizer, mse_history, dead_voxels).
+    """
     torch = _torch()
-    if psf.dims != bp.dims:
-        raise DimMismatch(f"PSF dims {psf.dims.shape} != backprojection dims {bp.dims.shape}")
-    if iterations < 1:
-        raise ValueError(f"iterations must be >= 1, got {iterations}")
-    _check_finite("image", image.data)
-    _check_finite("psf", psf.data)
-    _check_finite("backprojection", bp.data)
-    dev = f"cuda:{device}"
-    H = _to_device_f(psf.data, dev)
-    P = _to_device_f(bp.data, dev)
-    f = _to_device_f(image.data, dev, np.float64)
-    npx, npy = image.shape
-    n_z = psf.dims.n_z
-    odd = _odd(psf.dims.shape)
-    # odd sizes: forward through H' (pixel phase), backward through H (voxel
-    # phase) -- both coalesced gathers; even sizes: H forward, H' stamps back
+    dist = None
+    if sharded:
+        import torch.distributed as dist
 
-    def fwd(vol, out):
-        return forward_project_device(H, vol, out=out, Hp=P if odd else None)
-
-    def back(img, out):
-        return backproject_device(H, img, use_hprime=False, out=out) if odd else \
-            backproject_device(P, img, use_hprime=True, out=out)
-    norm = back(_to_device_f(np.ones((npx, npy)), dev), None)
-    peak = max(float(norm.max().item()), 0.0)
-    dead = int((norm < eps * peak).sum().item())
+    def allreduce(t, op):
+        if dist is not None:
+            dist.all_reduce(t, op=op, group=group)
+        return t
+    dev = f.device
+    npx, npy = f.shape
+    ones = _f_empty((npx, npy), dev)
+    ones.fill_(1.0)
+    norm = ops.back(ones, _f_empty((npx, npy, n_z), dev))
+    peak = torch.zeros(1, dtype=torch.float64, device=dev)
+    ops.max(norm, peak)
+    if dist is not None:
+        allreduce(peak, dist.ReduceOp.MAX)
+    dead_t = (norm < eps * peak).sum().to(torch.float64).reshape(1)
+    if dist is not None:
+        allreduce(dead_t, dist.ReduceOp.SUM)
+    dead = int(dead_t.item())
     if dead:
         log.warning("%d voxels receive no sensor coverage and stay zero", dead)
     g = _f_empty((npx, npy, n_z), dev)
@@ -226,16 +280,77 @@ def rl_run(psf, bp, image, iterations: int = 20, eps: float = 1e-12, device: int
     reproj = _f_empty((npx, npy), dev)
     ratio = _f_empty((npx, npy), dev)
     bwd = _f_empty((npx, npy, n_z), dev)
-    upd = _f_empty((npx, npy, n_z), dev)
-    scratch = torch.empty(1, dtype=torch.float64, device=dev)
+    rpeak = torch.zeros(1, dtype=torch.float64, device=dev)
+    ops.forward(g, reproj)
+    if dist is not None:
+        allreduce(reproj, dist.ReduceOp.SUM)
     mse = []
     for _ in range(iterations):
-        fwd(g, reproj)
-        safe_divide_device(f, reproj, eps, out=ratio, scratch=scratch)
-        back(ratio, bwd)
-        safe_divide_device(bwd, norm, eps, out=upd, scratch=scratch)
-        g.mul_(upd)
-        fwd(g, reproj)
+        ops.max(reproj, rpeak)
+        ops.divide(f, reproj, eps, rpeak, ratio)
+        ops.back(ratio, bwd)
+        ops.update(g, bwd, norm, eps, peak)
+        ops.forward(g, reproj)
+        if dist is not None:
+            allreduce(reproj, dist.ReduceOp.SUM)
         mse.append(((f - reproj) ** 2).mean())
     history = [float(v) for v in torch.stack(mse).cpu().tolist()]
+    return g, norm, history, dead
+
+
+def _rl_checks(psf, bp, image, iterations):
+    if psf.dims != bp.dims:
+        raise DimMismatch(f"PSF dims {psf.dims.shape} != backprojection dims {bp.dims.shape}")
+    if iterations < 1:
+        raise ValueError(f"iterations must be >= 1, got {iterations}")
+    _check_finite("image", image.data)
+    _check_finite("psf", psf.data)
+    _check_finite("backprojection", bp.data)
+
+
+def rl_run(psf, bp, image, iterations: int = 20, eps: float = 1e-12, device: int = 0) -> RlState:
+    """Richardson-Lucy deconvolution (projector.py:162-196) with all
+    projections and updates resident on the GPU."""
+    _rl_checks(psf, bp, image, iterations)
+    dev = f"cuda:{device}"
+    ops = DeviceSlabOps(_to_device_f(psf.data, dev), _to_device_f(bp.data, dev), _odd(psf.dims.shape))
+    f = _to_device_f(image.data, dev, np.float64)
+    g, norm, history, dead = rl_loop(ops, f, psf.dims.n_z, iterations, eps)
     return RlState(Volume._wrap(_to_host_f(g)), iterations, Volume._wrap(_to_host_f(norm)), history, dead)
+
+
+@dataclass
+class RlShard:
+    """One rank's share of a z-sharded RL run: planes [z0, z1) of the
+    estimate and normalizer; ``mse_history`` and ``dead_voxels`` are global."""
+    state: RlState
+    z0: int
+    z1: int
+
+
+def rl_run_sharded(psf, bp, image, iterations: int = 20, eps: float = 1e-12, group=None,
+                   device: int | None = None) -> RlShard:
+    """Richardson-Lucy with the depth planes sharded over the ranks of a
+    ``torch.distributed`` (NCCL) group, one GPU per rank.  Rank r moves only
+    its planes [z0, z1) (``shard.shard_planes``) of H and H' to its GPU; the
+    per-iteration exchange is one all-reduce of the partial forward
+    projection (see ``rl_loop``).  ``psf`` / ``bp`` may be memory-mapped:
+    only the rank's contiguous plane range is read."""
+    import torch.distributed as dist
+
+    from .shard import shard_planes
+    _rl_checks(psf, bp, image, iterations)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if device is None:
+        device = int(_torch().cuda.current_device())
+    z0, z1 = shard_planes(psf.dims.n_z, world, rank)
+    if z1 <= z0:
+        raise ValueError(f"rank {rank} of {world} gets no depth planes (n_z={psf.dims.n_z})")
+    dev = f"cuda:{device}"
+    ops = DeviceSlabOps(_to_device_f(psf.data[..., z0:z1], dev), _to_device_f(bp.data[..., z0:z1], dev),
+                        _odd(psf.dims.shape))
+    f = _to_device_f(image.data, dev, np.float64)
+    g, norm, history, dead = rl_loop(ops, f, z1 - z0, iterations, eps, sharded=world > 1, group=group)
+    st = RlState(Volume._wrap(_to_host_f(g)), iterations, Volume._wrap(_to_host_f(norm)), history, dead)
+    return RlShard(st, z0, z1)

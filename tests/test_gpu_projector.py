@@ -169,3 +169,74 @@ def test_random_shapes_match_oracle(shape, img):
     assert rel(forward_project(psf, Volume(g)).data, po.forward_project(H, g)) < 1e-12
     assert rel(backproject(bp, Image(f)).data, po.backproject(bp.data, f)) < 1e-12
     assert rel(backproject_adjoint(psf, Image(f)).data, po.backproject_adjoint(H, f)) < 1e-12
+
+
+def test_forward_projection_is_deterministic():
+    """rl_loop reuses the residual projection as the next iteration's
+    projection; that is exact only if a projection repeats bit for bit."""
+    torch = _torch()
+    from paper_2003_09133_b200.projector import _to_device_f, forward_project_device
+    from paper_2003_09133_b200.transform import hprime_device
+    rng = np.random.default_rng(3)
+    H = np.asfortranarray(rng.random((15, 13, 5, 3, 4)))
+    g = np.asfortranarray(rng.random((40, 33, 4)))
+    Hd, gd = _to_device_f(H, "cuda:0"), _to_device_f(g, "cuda:0")
+    Hp = hprime_device(Hd)
+    for kw in ({"Hp": Hp}, {}):
+        a = forward_project_device(Hd, gd, **kw).clone()
+        b = forward_project_device(Hd, gd, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+
+
+def test_rl_kernels_match_reference_safe_divide():
+    """lfbp_max_device / lfbp_safe_divide_peak_device / lfbp_rl_update_device
+    against _safe_divide (projector.py:135-145), including zero and tiny
+    denominators and an all-zero denominator (peak 0)."""
+    torch = _torch()
+    from paper_2003_09133_b200.projector import DeviceSlabOps
+    rng = np.random.default_rng(4)
+    num = rng.random(1000) * 3
+    for den in (rng.random(1000), np.zeros(1000)):
+        den = den.copy()
+        den[::7] = 0.0
+        den[::11] = 1e-15
+        nd, dd = torch.from_numpy(num).cuda(), torch.from_numpy(den).cuda()
+        peak = torch.zeros(1, dtype=torch.float64, device="cuda")
+        DeviceSlabOps.max(dd, peak)
+        assert float(peak.item()) == max(float(den.max()), 0.0)
+        out = DeviceSlabOps.divide(nd, dd, 1e-12, peak, torch.empty_like(nd))
+        want = po.safe_divide(num, den, 1e-12)
+        assert out.cpu().numpy().tobytes() == want.tobytes()
+        g0 = rng.random(1000)
+        g = torch.from_numpy(g0.copy()).cuda()
+        DeviceSlabOps.update(g, nd, dd, 1e-12, peak)
+        assert g.cpu().numpy().tobytes() == (g0 * want).tobytes()
+
+
+def test_rl_sharded_world_one_equals_rl_run(proj):
+    """rl_run_sharded through a 1-rank NCCL group (its plane-range slicing
+    and setup) gives the single-GPU rl_run result bit for bit."""
+    torch = _torch()
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2003_09133_b200.arrays import Image
+    from paper_2003_09133_b200.projector import rl_run, rl_run_sharded
+    psf, bp = _arrays(proj["rl6__H"])
+    img = Image(proj["rl6__f"])
+    want = rl_run(psf, bp, img, iterations=6)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        torch.cuda.set_device(0)
+        sh = rl_run_sharded(psf, bp, img, iterations=6)
+    finally:
+        dist.destroy_process_group()
+    assert (sh.z0, sh.z1) == (0, psf.dims.n_z)
+    assert sh.state.estimate.data.tobytes() == want.estimate.data.tobytes()
+    assert sh.state.mse_history == want.mse_history and sh.state.dead_voxels == want.dead_voxels

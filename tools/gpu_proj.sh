@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 420 python -m pytest tests -x -q -m gpu --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$? | tee -a gpurun_out/pytest_gpu.log
+timeout 300 python tools/proj_bench.py --psf C1 --image 256 > gpurun_out/proj_c1.json 2>&1
+timeout 600 python tools/proj_bench.py --psf C2 --image 512 --iters 3 > gpurun_out/proj_c2.json 2>&1
+true

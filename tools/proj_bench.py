@@ -53,19 +53,33 @@ def main():
     norm = backproject_device(Hp, torch.ones((N, N), dtype=torch.float64, device="cuda").t().contiguous().t())
     scratch = torch.empty(1, dtype=torch.float64, device="cuda")
 
-    def rl_iter():
+    def rl_iter():  # the pre-change loop body: fwd, divide, back, divide, mul, fwd
         reproj = forward_project_device(H, g, Hp=Hp)
         ratio = safe_divide_device(f, reproj, 1e-12, scratch=scratch)
         back = backproject_device(H, ratio, use_hprime=False)
         g.mul_(safe_divide_device(back, norm, 1e-12, scratch=scratch))
         forward_project_device(H, g, Hp=Hp)
-    t_rl = timed(rl_iter, a.iters)
+    t_rl_old = timed(rl_iter, a.iters)
+
+    from paper_2003_09133_b200.projector import DeviceSlabOps, rl_loop
+    ops = DeviceSlabOps(H, Hp, n_s % 2 == 1 and n_t % 2 == 1)
+
+    def rl_time(k):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rl_loop(ops, f, n_z, k, 1e-12)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+    rl_time(1)
+    t_rl = (rl_time(1 + a.iters) - rl_time(1)) / a.iters   # per iteration of the shipped loop
     x = torch.rand(8192, 8192, dtype=torch.float64, device="cuda")
     t_mm = timed(lambda: x @ x, 3)
     dgemm_tf = 2 * 8192 ** 3 / (t_mm * 1e-3) / 1e12
     res = {"psf": f"{w.name} {w.shape} {np.dtype(w.dtype).name}", "image": [N, N],
            "forward_ms": round(t_fwd, 3), "forward_H_form_ms": round(t_fwd_h, 3), "backproject_ms": round(t_bp, 3), "adjoint_ms": round(t_adj, 3),
-           "rl_iteration_ms": round(t_rl, 3),
+           "rl_iteration_ms": round(t_rl, 3), "rl_iteration_two_forward_ms": round(t_rl_old, 3),
            "forward_fp64_tflops": round(2 * macs / (t_fwd * 1e-3) / 1e12, 3),
            "backproject_fp64_tflops": round(2 * macs / (t_bp * 1e-3) / 1e12, 3),
            "adjoint_fp64_tflops": round(2 * macs / (t_adj * 1e-3) / 1e12, 3),
