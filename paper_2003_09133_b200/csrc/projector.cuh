@@ -200,20 +200,20 @@ __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict
     const int32_t ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
     const int32_t lyy = floordiv(rho_y, q.n_y) + pg.hy;
     const int32_t n_taps = (q.n_t - r2 + q.n_y - 1) / q.n_y;   // b = r2 + n_y * n < n_t
-    // tap a walks the sub-images rx = (px - c_s + a) mod n_x, stepping the
-    // coarse offset when rx wraps (no division in the loop)
+    // tap a reads sub-image rx = (px - c_s + a) mod n_x at coarse offset
+    // floordiv(px - c_s + a, n_x).  Taps are visited by residue class a0 of
+    // a mod n_x: within a class the sub-image is fixed and the coarse offset
+    // steps by one, so a block re-reads one small sub-image tile (L1 hits)
+    // instead of cycling through all n_x of them
     const int32_t rho0 = px - q.c_s;
-    int32_t rxx = ((rho0 % q.n_x) + q.n_x) % q.n_x;
-    int32_t kxx = floordiv(rho0, q.n_x) + pg.hx;
     const double* row0 = subz + int64_t(ryy) * q.n_x * sub_plane + k + int64_t(l0 + lyy) * pg.kp;
     const T* krow = Kz + int64_t(r2) * q.n_s;
-    for (int32_t a = 0; a < q.n_s; ++a) {
-      const double* col = row0 + int64_t(rxx) * sub_plane + kxx;
+    for (int32_t a0 = 0; a0 < q.n_x && a0 < q.n_s; ++a0) {
+    const int32_t rxx = (((rho0 + a0) % q.n_x) + q.n_x) % q.n_x;
+    const double* colx = row0 + int64_t(rxx) * sub_plane + floordiv(rho0 + a0, q.n_x) + pg.hx;
+    for (int32_t a = a0; a < q.n_s; a += q.n_x, ++colx) {
+      const double* col = colx;
       const T* kcol = krow + a;
-      if (++rxx == q.n_x) {
-        rxx = 0;
-        ++kxx;
-      }
       // register window over RL consecutive coarse rows, slid one row per
       // tap: blocks of RL taps use it as a circular buffer with static slot
       // indices (no moves), the remaining taps shift it
@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict
 #pragma unroll
         for (int j = 0; j < RL - 1; ++j) w[j] = w[j + 1];
       }
+    }
     }
   }
   const int32_t X = px + q.n_x * k;

@@ -61,19 +61,24 @@ def main():
         forward_project_device(H, g, Hp=Hp)
     t_rl_old = timed(rl_iter, a.iters)
 
-    from paper_2003_09133_b200.projector import DeviceSlabOps, rl_loop
+    from paper_2003_09133_b200.projector import DeviceSlabOps
     ops = DeviceSlabOps(H, Hp, n_s % 2 == 1 and n_t % 2 == 1)
+    peak = torch.zeros(1, dtype=torch.float64, device="cuda")
+    rpeak = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ops.max(norm, peak)
+    reproj = torch.empty_like(f)
+    ratio = torch.empty_like(f)
+    bwd = torch.empty_like(g)
+    ops.forward(g, reproj)
 
-    def rl_time(k):
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        rl_loop(ops, f, n_z, k, 1e-12)
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1)
-    rl_time(1)
-    t_rl = (rl_time(1 + a.iters) - rl_time(1)) / a.iters   # per iteration of the shipped loop
+    def rl_body():  # projector.rl_loop's iteration body, call for call
+        ops.max(reproj, rpeak)
+        ops.divide(f, reproj, 1e-12, rpeak, ratio)
+        ops.back(ratio, bwd)
+        ops.update(g, bwd, norm, 1e-12, peak)
+        ops.forward(g, reproj)
+        return ((f - reproj) ** 2).mean()
+    t_rl = timed(rl_body, a.iters)
     x = torch.rand(8192, 8192, dtype=torch.float64, device="cuda")
     t_mm = timed(lambda: x @ x, 3)
     dgemm_tf = 2 * 8192 ** 3 / (t_mm * 1e-3) / 1e12
