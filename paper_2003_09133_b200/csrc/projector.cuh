@@ -249,6 +249,128 @@ __global__ void __launch_bounds__(128) poly_corr_kernel(const double* __restrict
   }
 }
 
+// ---- shared-memory tiled polyphase correlation -----------------------------
+// Same sums as poly_corr_kernel, restructured around the fact that the taps of
+// one residue class (a = a0 + n_x a', b = r2 + n_y n) read ONE input
+// sub-image at consecutive coarse offsets.  A block owns one output phase
+// (px, py), one plane and a TK x (TLT*RL) coarse tile.  Per class pair
+// (r2, a0) it stages the sub-image window it needs (TK + M - 1 columns,
+// TLT*RL + N - 1 rows, zero outside the padded sub-image) and the M x N
+// class taps (converted to double once) in shared memory, then every thread
+// runs the register-window loop of poly_corr_kernel on shared memory: per tap
+// one LDS of the new window row, one broadcast LDS of the tap, RL DFMAs.
+struct PolyTile {
+  int32_t tk, tlt;     // block = tk x tlt threads (coarse x, groups of RL coarse rows)
+  int32_t tw, th, p;   // staged window: tw columns, th rows, row pitch p (doubles)
+  int32_t mmax, nmax;  // taps per class: ceil(n_s / n_x), ceil(n_t / n_y)
+};
+
+// resident blocks per SM the register budget is sized for: the RL
+// accumulators and the RL-row window dominate the register count
+constexpr int poly_tile_min_blocks(int rl) { return rl == 7 ? 7 : rl <= 8 ? 8 : rl <= 13 ? 5 : 4; }
+
+template <typename T, int RL>
+__global__ void __launch_bounds__(128, poly_tile_min_blocks(RL)) poly_tile_kernel(const double* __restrict__ sub, const T* __restrict__ K,
+                                                        double* __restrict__ out, const ProjGeom q, const PolyGeom pg,
+                                                        const PolyTile tg, int32_t forward) {
+  extern __shared__ double psm[];
+  double* tile = psm;                      // th x p
+  double* ks = psm + tg.th * tg.p;         // mmax x nmax
+  const int32_t nthr = tg.tk * tg.tlt;
+  const int32_t tid = threadIdx.x;
+  const int32_t tl = tid / tg.tk, tk = tid - tl * tg.tk;
+  const int32_t n_ph = q.n_x * q.n_y;
+  const int32_t ph = blockIdx.z % n_ph;
+  const int32_t zout = blockIdx.z / n_ph;
+  const int32_t px = ph % q.n_x, py = ph / q.n_x;
+  const int32_t k0 = blockIdx.x * tg.tk;
+  const int32_t L0 = blockIdx.y * tg.tlt * RL;
+  const int64_t pat = int64_t(q.n_s) * q.n_t;
+  const int64_t sub_plane = int64_t(pg.kp) * pg.lp;
+  const T* Kz = K + (int64_t(zout) * n_ph + ph) * pat;
+  const double* subz = sub + (forward ? int64_t(zout) * n_ph * sub_plane : 0);
+  const int32_t tiles = tg.tw * tg.th;
+  // fill walk: element tid, tid + nthr, ... of the tw x th window, as (row, col)
+  const int32_t dr = nthr / tg.tw, dc = nthr - dr * tg.tw;
+  const int32_t r_init = tid / tg.tw, c_init = tid - r_init * tg.tw;
+  double acc[RL];
+#pragma unroll
+  for (int j = 0; j < RL; ++j) acc[j] = 0.0;
+  const int32_t rho0 = px - q.c_s;
+  for (int32_t r2 = 0; r2 < q.n_y && r2 < q.n_t; ++r2) {
+    const int32_t rho_y = py - q.c_t + r2;
+    const int32_t ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
+    const int32_t row_base = floordiv(rho_y, q.n_y) + pg.hy + L0;
+    const int32_t N = (q.n_t - r2 + q.n_y - 1) / q.n_y;
+    for (int32_t a0 = 0; a0 < q.n_x && a0 < q.n_s; ++a0) {
+      const int32_t rxx = (((rho0 + a0) % q.n_x) + q.n_x) % q.n_x;
+      const int32_t col_base = floordiv(rho0 + a0, q.n_x) + pg.hx + k0;
+      const int32_t M = (q.n_s - a0 + q.n_x - 1) / q.n_x;
+      const double* sb = subz + (int64_t(ryy) * q.n_x + rxx) * sub_plane;
+      __syncthreads();  // the previous class's compute is done with tile / ks
+      {
+        int32_t r = r_init, c = c_init;
+        for (int32_t e = tid; e < tiles; e += nthr) {
+          const int32_t gr = row_base + r, gc = col_base + c;
+          double v = 0.0;
+          if (gr >= 0 && gr < pg.lp && gc >= 0 && gc < pg.kp) v = sb[gc + int64_t(gr) * pg.kp];
+          tile[r * tg.p + c] = v;
+          c += dc;
+          r += dr;
+          if (c >= tg.tw) {
+            c -= tg.tw;
+            ++r;
+          }
+        }
+      }
+      for (int32_t e = tid; e < tg.mmax * tg.nmax; e += nthr) {
+        const int32_t ap = e / tg.nmax, n = e - ap * tg.nmax;
+        double v = 0.0;
+        if (ap < M && n < N) v = static_cast<double>(Kz[(a0 + q.n_x * ap) + int64_t(q.n_s) * (r2 + q.n_y * n)]);
+        ks[e] = v;
+      }
+      __syncthreads();
+      for (int32_t ap = 0; ap < M; ++ap) {
+        const double* col = tile + (tl * RL) * tg.p + tk + ap;
+        const double* kv = ks + ap * tg.nmax;
+        double w[RL];
+#pragma unroll
+        for (int j = 0; j < RL - 1; ++j) w[j] = col[j * tg.p];
+        const double* rowp = col + (RL - 1) * tg.p;   // next window row to load
+        int32_t n = 0;
+        for (; n + RL <= N; n += RL) {
+#pragma unroll
+          for (int t = 0; t < RL; ++t) {
+            w[(RL - 1 + t) % RL] = *rowp;
+            rowp += tg.p;
+            const double v = kv[n + t];
+#pragma unroll
+            for (int j = 0; j < RL; ++j) acc[j] = fma(w[(j + t) % RL], v, acc[j]);
+          }
+        }
+        for (; n < N; ++n) {
+          w[RL - 1] = *rowp;
+          rowp += tg.p;
+          const double v = kv[n];
+#pragma unroll
+          for (int j = 0; j < RL; ++j) acc[j] = fma(w[j], v, acc[j]);
+#pragma unroll
+          for (int j = 0; j < RL - 1; ++j) w[j] = w[j + 1];
+        }
+      }
+    }
+  }
+  const int32_t k = k0 + tk;
+  const int32_t l = L0 + tl * RL;
+  const int32_t X = px + q.n_x * k;
+#pragma unroll
+  for (int j = 0; j < RL; ++j) {
+    const int32_t Y = py + q.n_y * (l + j);
+    if (k < pg.kc && l + j < pg.lc && X < q.nvx && Y < q.nvy)
+      out[X + int64_t(Y) * q.nvx + int64_t(zout) * q.nvx * q.nvy] = acc[j];
+  }
+}
+
 // forward: image = sum over z of the per-plane partial images (fixed order)
 __global__ void sum_planes_kernel(const double* __restrict__ part, double* __restrict__ out, int64_t n, int32_t planes) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
