@@ -80,7 +80,7 @@ def main():
               flush=True)
     del dev_a, dev_b
     ref = None
-    for mb in (16, 32, 64, 128, 256):
+    for mb in (34, 70):
         os.environ["LFBP_CHUNK_MB"] = str(mb)
 
         def call():
