@@ -4,7 +4,6 @@ back-to-back copies) -- the denominator K1 competes with at each size."""
 import json
 import os
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
