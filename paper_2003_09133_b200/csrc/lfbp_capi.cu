@@ -119,6 +119,16 @@ bool env_knobs_set() {
   return false;
 }
 
+constexpr int64_t kAutotuneMinBytes = int64_t(256) << 20;  // bytes moved (r+w) before the autotuner runs
+
+// Untuned knobs.  Below the autotuner's size a launch is latency-bound:
+// fewer, busier consumer warps per CTA and more CTAs (C1: 14.5 vs 17 us).
+Knobs default_knobs(int64_t moved_bytes) {
+  Knobs kn;
+  if (moved_bytes < kAutotuneMinBytes) kn.cwarps = 8;
+  return kn;
+}
+
 // Candidates tried by the autotuner (measured best plans of C1..C5 and
 // neighbours; every one is bit-exact, they differ only in speed).
 const Knobs kCandidates[] = {
@@ -216,7 +226,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   // lanes per output row: enough 16-byte groups per lane to amortise the row setup
   const int64_t groups = (std::min<int64_t>(p.C, d[0]) * E + 15) / 16 + 1;
   int W = env_int("LFBP_SUBWARP", kn.subwarp);
-  if (W != 8 && W != 16 && W != 32) W = groups <= 32 ? 8 : groups <= 64 ? 16 : 32;
+  if (W != 4 && W != 8 && W != 16 && W != 32) W = groups <= 16 ? 4 : groups <= 32 ? 8 : groups <= 64 ? 16 : 32;
   p.sub_width = W;
   p.gx_inc = static_cast<int32_t>((W * (16 / E)) % d[2]);
   p.nx_div = hp_fastdiv_make(static_cast<uint32_t>(d[2]));
@@ -415,7 +425,8 @@ int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dt
   if (!env_knobs_set()) {
     const TuneKey key{dims[0], dims[1], dims[2], dims[3], E, dev};
     const int64_t moved = 2 * plane_elems(dims) * (z_end - z_begin) * E;
-    if (!tuned_knobs(key, kn) && env_int("LFBP_AUTOTUNE", 1) && moved >= (int64_t(256) << 20)) {
+    kn = default_knobs(moved);
+    if (!tuned_knobs(key, kn) && env_int("LFBP_AUTOTUNE", 1) && moved >= kAutotuneMinBytes) {
       rc = autotune(key, src, dst, dims, E, z_begin, z_end - z_begin, total, static_cast<cudaStream_t>(stream), kn);
       if (rc) return rc;
     }
@@ -493,7 +504,7 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
     cudaGetDevice(&dev);
   }
   const int E = elem_size(dtype);
-  Knobs kn;
+  Knobs kn = default_knobs(2 * plane_elems(dims) * dims[4] * E);
   const bool tuned = !env_knobs_set() && tuned_knobs(TuneKey{dims[0], dims[1], dims[2], dims[3], E, dev}, kn);
   HpPlan p;
   rc = make_plan(p, dims, E, 0, dims[4], plane_elems(dims) * dims[4] * E, dev, kn);

@@ -3,14 +3,9 @@
 mkdir -p gpurun_out
 o=gpurun_out/c1_plans.txt; : > $o
 run() { echo "== $*" >> $o; env "$@" timeout 120 python bench.py --config C1 --steps 200 --no-cpu --no-e2e --no-verify 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); k=d['config']['kernel_plan']; print(d['roofline']['kernel_ms_avg'], d['value'], k['J'], k['stages'], k['threads'], k['ctas_per_sm'], k['grid'], k['n_units'])" >> $o; }
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); k=d['config']['kernel_plan']; print(d['roofline']['kernel_ms_avg'], d['value'], k['J'], k['stages'], k['threads'], k['ctas_per_sm'], k['grid'], k['n_units'], k['sub_width'])" >> $o; }
 run LFBP_X=0
-run LFBP_STAGE_KB=8 LFBP_STAGES=4 LFBP_CONSUMER_WARPS=4
-run LFBP_STAGE_KB=8 LFBP_STAGES=2 LFBP_CONSUMER_WARPS=4
-run LFBP_STAGE_KB=16 LFBP_STAGES=4 LFBP_CONSUMER_WARPS=8
-run LFBP_STAGE_KB=16 LFBP_STAGES=2 LFBP_CONSUMER_WARPS=8 LFBP_SUBWARP=8
-run LFBP_STAGE_KB=4 LFBP_STAGES=2 LFBP_CONSUMER_WARPS=2
-run LFBP_STAGE_KB=32 LFBP_STAGES=3 LFBP_CONSUMER_WARPS=12
-run LFBP_STAGE_KB=48 LFBP_STAGES=4 LFBP_CONSUMER_WARPS=12 LFBP_CTAS_PER_SM=1
-run LFBP_STAGE_KB=8 LFBP_STAGES=3 LFBP_CONSUMER_WARPS=8 LFBP_SUBWARP=8
+for W in 4 8; do for cw in 4 8 12; do for kb in 8 16 48; do
+run LFBP_SUBWARP=$W LFBP_CONSUMER_WARPS=$cw LFBP_STAGE_KB=$kb LFBP_STAGES=4
+done; done; done
 true
