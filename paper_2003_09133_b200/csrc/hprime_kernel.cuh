@@ -309,7 +309,7 @@ __device__ __forceinline__ void row_groups(typename Word<E>::T* o, int32_t g, in
 
 // Consumer warps (cw of nc) write the J * n_x output rows of the unit staged
 // at `stage` (smem address `stage_s`).  Each warp is split into 32/W
-// sub-warps of W = 4..32 lanes (p.sub_width); a sub-warp owns one output row at a
+// sub-warps of W = 2..32 lanes (p.sub_width); a sub-warp owns one output row at a
 // time, so the per-row index arithmetic is shared by 32/W rows and every
 // store instruction still writes W*16 contiguous bytes per row.  A row is cut
 // on the 16-byte grid of H' into groups of VE = 16/E elements; lane l of the
@@ -327,7 +327,7 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
   const int32_t n_x = static_cast<int32_t>(p.n_x);
   const int32_t n_s = static_cast<int32_t>(p.n_s);
   const int32_t W = p.sub_width;
-  const int32_t lw = W == 4 ? 2 : W == 8 ? 3 : W == 16 ? 4 : 5;  // log2(W): no integer division below
+  const int32_t lw = W == 2 ? 1 : W == 4 ? 2 : W == 8 ? 3 : W == 16 ? 4 : 5;  // log2(W): no division below
   const int32_t sl = lane & (W - 1);               // lane within the sub-warp
   const int32_t R = 32 >> lw;                      // rows in flight per warp
   const int32_t rp = p.row_pitch;

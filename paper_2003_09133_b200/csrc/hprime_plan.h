@@ -89,7 +89,7 @@ struct HpPlan {
   int32_t ctas_per_sm;
   int32_t xs16;               // (n_s * n_t * elem) mod 16: run misalignment step per x
   int32_t flags;              // HP_FLAG_*
-  int32_t sub_width;          // lanes per output row (4, 8, 16 or 32)
+  int32_t sub_width;          // lanes per output row (2, 4, 8, 16 or 32)
   int32_t gx_inc;             // (sub_width * 16/elem) mod n_x: phase advance of one stride
   int64_t n_units;            // z_count * n_chunks * n_bands * n_y  (< 2^31)
   HpFastDiv nx_div;           // mod n_x on the element path

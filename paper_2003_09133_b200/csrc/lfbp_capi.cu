@@ -226,7 +226,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   // lanes per output row: enough 16-byte groups per lane to amortise the row setup
   const int64_t groups = (std::min<int64_t>(p.C, d[0]) * E + 15) / 16 + 1;
   int W = env_int("LFBP_SUBWARP", kn.subwarp);
-  if (W != 4 && W != 8 && W != 16 && W != 32) W = groups <= 16 ? 4 : groups <= 32 ? 8 : groups <= 64 ? 16 : 32;
+  if (W != 2 && W != 4 && W != 8 && W != 16 && W != 32) W = groups <= 16 ? 4 : groups <= 32 ? 8 : groups <= 64 ? 16 : 32;
   p.sub_width = W;
   p.gx_inc = static_cast<int32_t>((W * (16 / E)) % d[2]);
   p.nx_div = hp_fastdiv_make(static_cast<uint32_t>(d[2]));

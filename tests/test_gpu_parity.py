@@ -151,7 +151,7 @@ def test_random_shapes_match_oracle(shape, dtype):
     {"LFBP_STAGES": "1"}, {"LFBP_STAGES": "2", "LFBP_CONSUMER_WARPS": "1"},
     {"LFBP_STAGE_KB": "1"}, {"LFBP_STAGE_KB": "200", "LFBP_STAGE_MAX_KB": "200"},
     {"LFBP_CTAS_PER_SM": "1", "LFBP_CONSUMER_WARPS": "16"}, {"LFBP_BAND": "3"},
-    {"LFBP_SUBWARP": "4"}, {"LFBP_SUBWARP": "8"}, {"LFBP_SUBWARP": "32"},
+    {"LFBP_SUBWARP": "2"}, {"LFBP_SUBWARP": "4"}, {"LFBP_SUBWARP": "8"}, {"LFBP_SUBWARP": "32"},
     {"LFBP_SUBWARP": "16", "LFBP_CONSUMER_WARPS": "3"}, {"LFBP_SUBWARP": "4", "LFBP_STAGE_MAX_KB": "2"},
     {"LFBP_SUBWARP": "8", "LFBP_STAGE_MAX_KB": "2", "LFBP_STAGES": "2"},
 ])
