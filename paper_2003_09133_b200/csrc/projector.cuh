@@ -267,7 +267,7 @@ struct PolyTile {
 
 // resident blocks per SM the register budget is sized for: the RL
 // accumulators and the RL-row window dominate the register count
-constexpr int poly_tile_min_blocks(int rl) { return rl == 7 ? 7 : rl <= 8 ? 8 : rl <= 13 ? 5 : 4; }
+constexpr int poly_tile_min_blocks(int rl) { return rl == 7 ? 7 : rl <= 8 ? 8 : rl == 12 ? 5 : rl <= 13 ? 6 : 4; }
 
 template <typename T, int RL>
 __global__ void __launch_bounds__(128, poly_tile_min_blocks(RL)) poly_tile_kernel(const double* __restrict__ sub, const T* __restrict__ K,
