@@ -372,7 +372,8 @@ def main():
                          "kernel": "hp::hprime_kernel (K1)", "kernel_ms_avg": round(avg_kern_ms, 4),
                          "kernel_ms_min": round(min(kern_ms), 4),
                          "algorithmic_bytes_per_launch": step_bytes},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "first_timed_launch": l0,
+            "clocks": clk.summary(),
             "verified_vs_reference_digests": verified,
         }
         print(json.dumps(line), flush=True)

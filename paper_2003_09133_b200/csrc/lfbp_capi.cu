@@ -285,29 +285,55 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
   HP_CUDA(cudaEventCreate(&e0));
   HP_CUDA(cudaEventCreate(&e1));
   // candidates interleaved over rounds (decorrelates clock / power drift);
-  // score = median of the per-round launch times
+  // each measurement is `reps` back-to-back launches (>= ~8 ms, so a plan is
+  // judged at its steady-state rate, not on one launch after an idle gap);
+  // score = median over rounds of the per-launch time
   constexpr int kCand = int(sizeof(kCandidates) / sizeof(kCandidates[0]));
   constexpr int kRounds = 3;
   HpPlan plans[kCand];
   bool ok[kCand];
   float t[kCand][kRounds];
+  cudaEvent_t ev[kCand][2];
+  for (int c = 0; c < kCand; ++c) {
+    HP_CUDA(cudaEventCreate(&ev[c][0]));
+    HP_CUDA(cudaEventCreate(&ev[c][1]));
+  }
+  float warm_ms = 0.f;
   for (int c = 0; c < kCand; ++c) {
     ok[c] = make_plan(plans[c], dims, E, z_begin, z_count, total, key.dev, kCandidates[c]) == LFBP_OK;
     if (ok[c]) {
-      int rc = launch(plans[c], src, dst, st);  // warm
-      if (rc) return rc;
-    }
-  }
-  for (int r = 0; r < kRounds; ++r)
-    for (int c = 0; c < kCand; ++c) {
-      if (!ok[c]) continue;
       HP_CUDA(cudaEventRecord(e0, st));
-      int rc = launch(plans[c], src, dst, st);
+      int rc = launch(plans[c], src, dst, st);  // warm
       if (rc) return rc;
       HP_CUDA(cudaEventRecord(e1, st));
       HP_CUDA(cudaEventSynchronize(e1));
-      HP_CUDA(cudaEventElapsedTime(&t[c][r], e0, e1));
+      float ms = 0.f;
+      HP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      warm_ms = std::max(warm_ms, ms);
     }
+  }
+  const int reps = std::max(1, std::min(64, int(8.0f / std::max(warm_ms, 1e-3f))));
+  for (int r = 0; r < kRounds; ++r) {
+    for (int c = 0; c < kCand; ++c) {
+      if (!ok[c]) continue;
+      HP_CUDA(cudaEventRecord(ev[c][0], st));
+      for (int k = 0; k < reps; ++k) {
+        int rc = launch(plans[c], src, dst, st);
+        if (rc) return rc;
+      }
+      HP_CUDA(cudaEventRecord(ev[c][1], st));
+    }
+    HP_CUDA(cudaStreamSynchronize(st));
+    for (int c = 0; c < kCand; ++c) {
+      if (!ok[c]) continue;
+      HP_CUDA(cudaEventElapsedTime(&t[c][r], ev[c][0], ev[c][1]));
+      t[c][r] /= float(reps);
+    }
+  }
+  for (int c = 0; c < kCand; ++c) {
+    cudaEventDestroy(ev[c][0]);
+    cudaEventDestroy(ev[c][1]);
+  }
   float best_ms = 1e30f;
   bool found = false;
   for (int c = 0; c < kCand; ++c) {
@@ -514,10 +540,12 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
                    "{\"elem\": %d, \"J\": %d, \"n_bands\": %d, \"C\": %d, \"n_chunks\": %d, \"row_pitch\": %d, "
                    "\"stage_bytes\": %d, \"stages\": %d, \"threads\": %d, \"smem_bytes\": %d, \"ctas_per_sm\": %d, "
                    "\"grid\": %d, \"n_units\": %lld, \"sub_width\": %d, \"sm_count\": %d, \"device_props\": \"%s\", "
-                   "\"autotuned\": %s}",
+                   "\"autotuned\": %s, \"knobs\": [%d, %d, %d, %d]}",
                    p.elem, p.J, p.n_bands, p.C, p.n_chunks, p.row_pitch, p.stage_bytes, p.stages, p.threads,
                    p.smem_bytes, p.ctas_per_sm, p.grid, (long long)p.n_units, p.sub_width, dp.sm_count,
-                   dp.real ? "queried" : "b200-defaults", tuned ? "true" : "false");
+                   dp.real ? "queried" : "b200-defaults", tuned ? "true" : "false",
+                   env_int("LFBP_STAGES", kn.stages), env_int("LFBP_STAGE_KB", kn.stage_kb),
+                   env_int("LFBP_CONSUMER_WARPS", kn.cwarps), env_int("LFBP_SUBWARP", kn.subwarp));
   if (w < 0 || w >= buf_len) return fail(LFBP_ERR_ARGUMENT, "buffer too small");
   return LFBP_OK;
 }
