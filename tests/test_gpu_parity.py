@@ -335,3 +335,29 @@ def test_cuda_graph_capture_and_replay():
         g.replay()
     torch.cuda.synchronize()
     assert to_host(out).tobytes() == fbytes(hprime_oracle(H))
+
+
+def test_autotuner_picks_a_candidate_and_stays_exact(monkeypatch):
+    """A call moving >= 256 MB autotunes once: the cached plan is one of the
+    candidates, later calls reuse it, and the result (written by the last
+    candidate timed, then the chosen plan) is exact -- checked through the
+    involution H'' == H on the device.  A capturing stream skips tuning."""
+    torch = _torch()
+    from paper_2003_09133_b200 import f_order_empty, hprime_device, plan
+    from paper_2003_09133_b200.verify import compare_device
+    for k in ("LFBP_STAGES", "LFBP_STAGE_KB", "LFBP_CONSUMER_WARPS", "LFBP_SUBWARP", "LFBP_AUTOTUNE"):
+        monkeypatch.delenv(k, raising=False)
+    shape = (197, 193, 15, 13, 5)               # a plane shape no other test tunes; 2 x 190 MB moved
+    src = f_order_empty(shape, torch.float32)
+    src.permute(4, 3, 2, 1, 0).reshape(-1).uniform_()
+    assert plan(shape)["autotuned"] is False
+    out = hprime_device(src)
+    p = plan(shape)
+    assert p["autotuned"] is True
+    candidates = {(3, 48, 8, 8), (4, 48, 12, 16), (4, 48, 8, 8), (4, 48, 8, 16), (2, 96, 8, 16), (3, 64, 8, 32),
+                  (4, 48, 16, 16), (2, 96, 8, 8)}
+    assert tuple(p["knobs"]) in candidates
+    back = hprime_device(out, inverse=True)
+    n_diff, _ = compare_device(back, src)
+    assert n_diff == 0
+    torch.cuda.synchronize()
