@@ -119,9 +119,15 @@ bool env_knobs_set() {
   return false;
 }
 
-constexpr int64_t kAutotuneMinBytes = int64_t(256) << 20;  // bytes moved (r+w) before the autotuner runs
+constexpr int64_t kAutotuneMinBytes = int64_t(256) << 20;  // bytes moved (r+w): large-problem candidates
+constexpr int64_t kSmallTuneMinBytes = int64_t(8) << 20;   // ... small-problem candidates from here
 
-// Untuned knobs.  Below the autotuner's size a launch is latency-bound:
+// Size class of a launch for the tuner: 1 large, 0 small, -1 not tuned.
+int tune_class(int64_t moved_bytes) {
+  return moved_bytes >= kAutotuneMinBytes ? 1 : moved_bytes >= kSmallTuneMinBytes ? 0 : -1;
+}
+
+// Untuned knobs.  Below the large-problem size a launch is latency-bound:
 // fewer, busier consumer warps per CTA and more CTAs (C1: 14.5 vs 17 us).
 Knobs default_knobs(int64_t moved_bytes) {
   Knobs kn;
@@ -132,9 +138,19 @@ Knobs default_knobs(int64_t moved_bytes) {
 // Candidates tried by the autotuner (measured best plans of C1..C5 and
 // neighbours; every one is bit-exact, they differ only in speed).
 const Knobs kCandidates[] = {
-    {3, 48, 8, 8},  {4, 48, 12, 16}, {4, 48, 8, 8},  {4, 48, 8, 16},
-    {2, 96, 8, 16}, {3, 64, 8, 32},  {4, 48, 16, 16}, {2, 96, 8, 8},
+    {3, 48, 8, 8},  {4, 48, 12, 16}, {4, 48, 8, 8},  {4, 48, 8, 16}, {2, 96, 8, 16},
+    {3, 64, 8, 32}, {4, 48, 16, 16}, {2, 96, 8, 8},  {4, 16, 8, 0},  {4, 16, 4, 4},
 };
+// Small problems (8-256 MB moved) are latency-bound: smaller stages (narrower
+// t-bands, several CTAs per SM) and short-row sub-warps; measured on the
+// paper's small Table 1 geometries and C1 (profiles/r01_small_shapes.jsonl).
+const Knobs kSmallCandidates[] = {
+    {4, 48, 8, 0}, {4, 16, 8, 0}, {4, 16, 4, 4}, {4, 8, 8, 4},
+    {4, 24, 8, 0}, {4, 32, 8, 0}, {4, 12, 4, 4}, {4, 16, 8, 8},
+};
+constexpr int kNumCandidates = int(sizeof(kCandidates) / sizeof(kCandidates[0]));
+constexpr int kNumSmallCandidates = int(sizeof(kSmallCandidates) / sizeof(kSmallCandidates[0]));
+static_assert(kNumSmallCandidates <= kNumCandidates, "arrays in autotune() are sized by the large set");
 
 // Work-unit shape, smem ring and persistent grid for one launch.
 int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_count,
@@ -253,12 +269,14 @@ int launch(const HpPlan& p, const void* src, void* dst, cudaStream_t st) {
 struct TuneKey {
   int64_t n_s, n_t, n_x, n_y;
   int E, dev;
+  int cls;  // tune_class of the launch size: small and large launches tune separately
   bool operator<(const TuneKey& o) const {
     if (n_s != o.n_s) return n_s < o.n_s;
     if (n_t != o.n_t) return n_t < o.n_t;
     if (n_x != o.n_x) return n_x < o.n_x;
     if (n_y != o.n_y) return n_y < o.n_y;
     if (E != o.E) return E < o.E;
+    if (cls != o.cls) return cls < o.cls;
     return dev < o.dev;
   }
 };
@@ -288,10 +306,12 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
   // each measurement is `reps` back-to-back launches (>= ~8 ms, so a plan is
   // judged at its steady-state rate, not on one launch after an idle gap);
   // score = median over rounds of the per-launch time
-  constexpr int kCand = int(sizeof(kCandidates) / sizeof(kCandidates[0]));
+  constexpr int kCand = kNumCandidates;
   constexpr int kRounds = 3;
+  const Knobs* cand = key.cls == 1 ? kCandidates : kSmallCandidates;
+  const int n_cand = key.cls == 1 ? kNumCandidates : kNumSmallCandidates;
   HpPlan plans[kCand];
-  bool ok[kCand];
+  bool ok[kCand] = {};
   float t[kCand][kRounds];
   cudaEvent_t ev[kCand][2];
   for (int c = 0; c < kCand; ++c) {
@@ -299,8 +319,8 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
     HP_CUDA(cudaEventCreate(&ev[c][1]));
   }
   float warm_ms = 0.f;
-  for (int c = 0; c < kCand; ++c) {
-    ok[c] = make_plan(plans[c], dims, E, z_begin, z_count, total, key.dev, kCandidates[c]) == LFBP_OK;
+  for (int c = 0; c < n_cand; ++c) {
+    ok[c] = make_plan(plans[c], dims, E, z_begin, z_count, total, key.dev, cand[c]) == LFBP_OK;
     if (ok[c]) {
       HP_CUDA(cudaEventRecord(e0, st));
       int rc = launch(plans[c], src, dst, st);  // warm
@@ -314,7 +334,7 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
   }
   const int reps = std::max(1, std::min(64, int(8.0f / std::max(warm_ms, 1e-3f))));
   for (int r = 0; r < kRounds; ++r) {
-    for (int c = 0; c < kCand; ++c) {
+    for (int c = 0; c < n_cand; ++c) {
       if (!ok[c]) continue;
       HP_CUDA(cudaEventRecord(ev[c][0], st));
       for (int k = 0; k < reps; ++k) {
@@ -324,7 +344,7 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
       HP_CUDA(cudaEventRecord(ev[c][1], st));
     }
     HP_CUDA(cudaStreamSynchronize(st));
-    for (int c = 0; c < kCand; ++c) {
+    for (int c = 0; c < n_cand; ++c) {
       if (!ok[c]) continue;
       HP_CUDA(cudaEventElapsedTime(&t[c][r], ev[c][0], ev[c][1]));
       t[c][r] /= float(reps);
@@ -336,14 +356,14 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
   }
   float best_ms = 1e30f;
   bool found = false;
-  for (int c = 0; c < kCand; ++c) {
+  for (int c = 0; c < n_cand; ++c) {
     if (!ok[c]) continue;
     float v[kRounds];
     for (int r = 0; r < kRounds; ++r) v[r] = t[c][r];
     std::sort(v, v + kRounds);
     if (v[kRounds / 2] < best_ms) {
       best_ms = v[kRounds / 2];
-      best = kCandidates[c];
+      best = cand[c];
       found = true;
     }
   }
@@ -449,10 +469,10 @@ int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dt
   HP_CUDA(cudaGetDevice(&dev));
   Knobs kn;
   if (!env_knobs_set()) {
-    const TuneKey key{dims[0], dims[1], dims[2], dims[3], E, dev};
     const int64_t moved = 2 * plane_elems(dims) * (z_end - z_begin) * E;
+    const TuneKey key{dims[0], dims[1], dims[2], dims[3], E, dev, tune_class(moved)};
     kn = default_knobs(moved);
-    if (!tuned_knobs(key, kn) && env_int("LFBP_AUTOTUNE", 1) && moved >= kAutotuneMinBytes) {
+    if (key.cls >= 0 && !tuned_knobs(key, kn) && env_int("LFBP_AUTOTUNE", 1)) {
       rc = autotune(key, src, dst, dims, E, z_begin, z_end - z_begin, total, static_cast<cudaStream_t>(stream), kn);
       if (rc) return rc;
     }
@@ -530,8 +550,10 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
     cudaGetDevice(&dev);
   }
   const int E = elem_size(dtype);
-  Knobs kn = default_knobs(2 * plane_elems(dims) * dims[4] * E);
-  const bool tuned = !env_knobs_set() && tuned_knobs(TuneKey{dims[0], dims[1], dims[2], dims[3], E, dev}, kn);
+  const int64_t moved = 2 * plane_elems(dims) * dims[4] * E;
+  Knobs kn = default_knobs(moved);
+  const bool tuned =
+      !env_knobs_set() && tuned_knobs(TuneKey{dims[0], dims[1], dims[2], dims[3], E, dev, tune_class(moved)}, kn);
   HpPlan p;
   rc = make_plan(p, dims, E, 0, dims[4], plane_elems(dims) * dims[4] * E, dev, kn);
   if (rc) return rc;

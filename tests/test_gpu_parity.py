@@ -355,7 +355,7 @@ def test_autotuner_picks_a_candidate_and_stays_exact(monkeypatch):
     p = plan(shape)
     assert p["autotuned"] is True
     candidates = {(3, 48, 8, 8), (4, 48, 12, 16), (4, 48, 8, 8), (4, 48, 8, 16), (2, 96, 8, 16), (3, 64, 8, 32),
-                  (4, 48, 16, 16), (2, 96, 8, 8)}
+                  (4, 48, 16, 16), (2, 96, 8, 8), (4, 16, 8, 0), (4, 16, 4, 4)}
     assert tuple(p["knobs"]) in candidates
     back = hprime_device(out, inverse=True)
     n_diff, _ = compare_device(back, src)

@@ -20,6 +20,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--secs", type=float, default=0.3)
     ap.add_argument("--nz", type=int, default=11)
+    ap.add_argument("--only", default="", help="comma-separated indices into SHAPES")
+    ap.add_argument("--tag", default="")
     a = ap.parse_args()
     import torch
 
@@ -40,7 +42,8 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps
-    for s4 in SHAPES:
+    shapes = [SHAPES[int(i)] for i in a.only.split(",")] if a.only else SHAPES
+    for s4 in shapes:
         shape = s4 + (a.nz,)
         src = f_order_empty(shape, torch.float32)
         src.permute(4, 3, 2, 1, 0).reshape(-1).uniform_()
@@ -50,7 +53,7 @@ def main():
         cms = timed(lambda: fo.copy_(fs))
         nb = 2 * src.numel() * 4
         p = plan(shape)
-        print(json.dumps({"shape": shape, "plane_mb": round(src.numel() * 4 / a.nz / 1e6, 1), "ms": round(ms, 4),
+        print(json.dumps({"tag": a.tag, "shape": shape, "plane_mb": round(src.numel() * 4 / a.nz / 1e6, 1), "ms": round(ms, 4),
                           "GBps": round(nb / ms / 1e6, 1), "copy_GBps": round(nb / cms / 1e6, 1),
                           "frac_of_copy": round(cms / ms, 3), "Gelem_s": round(src.numel() / ms / 1e6, 1),
                           "knobs": p["knobs"], "J": p["J"], "n_chunks": p["n_chunks"]}), flush=True)
