@@ -299,9 +299,21 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   HP_CUDA(cudaStreamIsCapturing(st, &cs));
   if (cs != cudaStreamCaptureStatusNone) return LFBP_OK;
+  // every event this function creates is destroyed on every return path
+  struct Events {
+    std::vector<cudaEvent_t> v;
+    cudaError_t make(cudaEvent_t* e) {
+      cudaError_t r = cudaEventCreate(e);
+      if (r == cudaSuccess) v.push_back(*e);
+      return r;
+    }
+    ~Events() {
+      for (cudaEvent_t e : v) cudaEventDestroy(e);
+    }
+  } events;
   cudaEvent_t e0, e1;
-  HP_CUDA(cudaEventCreate(&e0));
-  HP_CUDA(cudaEventCreate(&e1));
+  HP_CUDA(events.make(&e0));
+  HP_CUDA(events.make(&e1));
   // candidates interleaved over rounds (decorrelates clock / power drift);
   // each measurement is `reps` back-to-back launches (>= ~8 ms, so a plan is
   // judged at its steady-state rate, not on one launch after an idle gap);
@@ -314,9 +326,9 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
   bool ok[kCand] = {};
   float t[kCand][kRounds];
   cudaEvent_t ev[kCand][2];
-  for (int c = 0; c < kCand; ++c) {
-    HP_CUDA(cudaEventCreate(&ev[c][0]));
-    HP_CUDA(cudaEventCreate(&ev[c][1]));
+  for (int c = 0; c < n_cand; ++c) {
+    HP_CUDA(events.make(&ev[c][0]));
+    HP_CUDA(events.make(&ev[c][1]));
   }
   float warm_ms = 0.f;
   for (int c = 0; c < n_cand; ++c) {
@@ -350,10 +362,6 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
       t[c][r] /= float(reps);
     }
   }
-  for (int c = 0; c < kCand; ++c) {
-    cudaEventDestroy(ev[c][0]);
-    cudaEventDestroy(ev[c][1]);
-  }
   float best_ms = 1e30f;
   bool found = false;
   for (int c = 0; c < n_cand; ++c) {
@@ -367,8 +375,6 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
       found = true;
     }
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   g_err.clear();
   if (found) {
     std::lock_guard<std::mutex> lk(g_tune_mu);
