@@ -263,6 +263,8 @@ struct PolyTile {
   int32_t tk, tlt;     // block = tk x tlt threads (coarse x, groups of RL coarse rows)
   int32_t tw, th, p;   // staged window: tw columns, th rows, row pitch p (doubles)
   int32_t mmax, nmax;  // taps per class: ceil(n_s / n_x), ceil(n_t / n_y)
+  int32_t conv;        // 0: correlation, K phase = output phase (H' forward, adjoint);
+                       // 1: convolution, K phase = input phase (H forward, H'-stamp backprojection)
 };
 
 // resident blocks per SM the register budget is sized for: the RL
@@ -298,15 +300,21 @@ __global__ void __launch_bounds__(128, poly_tile_min_blocks(RL)) poly_tile_kerne
   for (int j = 0; j < RL; ++j) acc[j] = 0.0;
   const int32_t rho0 = px - q.c_s;
   for (int32_t r2 = 0; r2 < q.n_y && r2 < q.n_t; ++r2) {
-    const int32_t rho_y = py - q.c_t + r2;
-    const int32_t ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
-    const int32_t row_base = floordiv(rho_y, q.n_y) + pg.hy + L0;
     const int32_t N = (q.n_t - r2 + q.n_y - 1) / q.n_y;
+    // correlation: tap b = r2 + n_y n reads input row l + floordiv(py - c_t + r2, n_y) + n;
+    // convolution: it reads l + floordiv(py + c_t - r2, n_y) - n, staged with the taps
+    // reversed (nn = N - 1 - n) so the compute loop below is the same
+    const int32_t rho_y = tg.conv ? py + q.c_t - r2 : py - q.c_t + r2;
+    const int32_t ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
+    const int32_t row_base = floordiv(rho_y, q.n_y) + pg.hy + L0 - (tg.conv ? N - 1 : 0);
     for (int32_t a0 = 0; a0 < q.n_x && a0 < q.n_s; ++a0) {
-      const int32_t rxx = (((rho0 + a0) % q.n_x) + q.n_x) % q.n_x;
-      const int32_t col_base = floordiv(rho0 + a0, q.n_x) + pg.hx + k0;
       const int32_t M = (q.n_s - a0 + q.n_x - 1) / q.n_x;
+      const int32_t rho_x = tg.conv ? px + q.c_s - a0 : rho0 + a0;
+      const int32_t rxx = ((rho_x % q.n_x) + q.n_x) % q.n_x;
+      const int32_t col_base = floordiv(rho_x, q.n_x) + pg.hx + k0 - (tg.conv ? M - 1 : 0);
       const double* sb = subz + (int64_t(ryy) * q.n_x + rxx) * sub_plane;
+      // convolution: the pattern of the class is the input phase's, H[., ., rxx, ryy, z]
+      const T* Kc = tg.conv ? K + (int64_t(zout) * n_ph + rxx + int64_t(q.n_x) * ryy) * pat : Kz;
       __syncthreads();  // the previous class's compute is done with tile / ks
       {
         int32_t r = r_init, c = c_init;
@@ -326,7 +334,10 @@ __global__ void __launch_bounds__(128, poly_tile_min_blocks(RL)) poly_tile_kerne
       for (int32_t e = tid; e < tg.mmax * tg.nmax; e += nthr) {
         const int32_t ap = e / tg.nmax, n = e - ap * tg.nmax;
         double v = 0.0;
-        if (ap < M && n < N) v = static_cast<double>(Kz[(a0 + q.n_x * ap) + int64_t(q.n_s) * (r2 + q.n_y * n)]);
+        if (ap < M && n < N) {
+          const int32_t ta = tg.conv ? M - 1 - ap : ap, tb = tg.conv ? N - 1 - n : n;
+          v = static_cast<double>(Kc[(a0 + q.n_x * ta) + int64_t(q.n_s) * (r2 + q.n_y * tb)]);
+        }
         ks[e] = v;
       }
       __syncthreads();

@@ -240,3 +240,51 @@ def test_rl_sharded_world_one_equals_rl_run(proj):
     assert (sh.z0, sh.z1) == (0, psf.dims.n_z)
     assert sh.state.estimate.data.tobytes() == want.estimate.data.tobytes()
     assert sh.state.mse_history == want.mse_history and sh.state.dead_voxels == want.dead_voxels
+
+
+@pytest.mark.parametrize("shape,img", [((15, 13, 5, 3, 2), (40, 33)), ((8, 12, 7, 3, 2), (20, 17)),
+                                       ((20, 18, 5, 7, 3), (33, 41)), ((33, 31, 11, 3, 2), (70, 23))])
+def test_both_polyphase_forms_match_oracle(shape, img):
+    """Every device form against the oracle, odd and even sizes: the H form
+    of the forward projection and the H'-stamp backprojection run as
+    polyphase convolutions (input-phase patterns), the H' forward and the
+    adjoint as polyphase correlations (output-phase patterns)."""
+    torch = _torch()
+    from oracle.hprime_oracle import hprime_oracle
+    from paper_2003_09133_b200.projector import (_to_device_f, _to_host_f, backproject_device,
+                                                 forward_project_device)
+    from paper_2003_09133_b200.synth import random_psf_like_reference as rpsf
+    H = np.asfortranarray(rpsf(shape, density=0.7, seed=11, dtype=np.float64))
+    Hp = np.asfortranarray(hprime_oracle(H))
+    rng = np.random.default_rng(5)
+    g = np.asfortranarray(rng.random((*img, shape[4])))
+    f = np.asfortranarray(rng.random(img))
+    Hd, Hpd = _to_device_f(H, "cuda:0"), _to_device_f(Hp, "cuda:0")
+    gd, fd = _to_device_f(g, "cuda:0"), _to_device_f(f, "cuda:0")
+    want_fwd = po.forward_project(H, g)
+    assert rel(_to_host_f(forward_project_device(Hd, gd)), want_fwd) < 1e-12           # H form (convolution)
+    if shape[0] % 2 and shape[1] % 2:
+        assert rel(_to_host_f(forward_project_device(None, gd, Hp=Hpd)), want_fwd) < 1e-12   # H' form
+    assert rel(_to_host_f(backproject_device(Hpd, fd, use_hprime=True)), po.backproject(Hp, f)) < 1e-12
+    assert rel(_to_host_f(backproject_device(Hd, fd, use_hprime=False)), po.backproject_adjoint(H, f)) < 1e-12
+    torch.cuda.synchronize()
+
+
+def test_rl_even_sizes_match_oracle():
+    """RL with even n_s, n_t (H forward and H'-stamp backward, both polyphase
+    convolutions on the device) against the oracle's RL."""
+    _torch()
+    from paper_2003_09133_b200 import Dims5, PsfArray, compute_backprojection
+    from paper_2003_09133_b200.arrays import Image
+    from paper_2003_09133_b200.projector import rl_run
+    from paper_2003_09133_b200.synth import random_psf_like_reference as rpsf
+    shape = (12, 10, 5, 3, 3)
+    H = rpsf(shape, density=0.8, seed=9, dtype=np.float64)
+    psf = PsfArray._wrap(Dims5(*shape), H)
+    bp = compute_backprojection(psf)
+    f = np.random.default_rng(2).random((25, 19)) + 0.05
+    st = rl_run(psf, bp, Image(f), iterations=4)
+    g_ref, hist_ref, norm_ref = po.rl_run(H, bp.data, f, iterations=4)
+    assert rel(st.normalizer.data, norm_ref) < 1e-12
+    assert rel(st.estimate.data, g_ref) < 1e-10
+    assert np.allclose(st.mse_history, hist_ref, rtol=1e-10, atol=0)
