@@ -139,17 +139,15 @@ def safe_divide_device(num, den, eps: float, out=None, scratch=None):
 # drop-ins for the reference's host API
 
 def forward_project(psf, volume, device: int = 0) -> Image:
-    """projector.py:55-81 on the GPU (H' computed on the device for the
-    pixel-phase gather when n_s, n_t are odd)."""
-    from .transform import hprime_device
+    """projector.py:55-81 on the GPU: the H-form sums as a polyphase
+    convolution over H (the pattern of a tap class is the voxel's phase)."""
     n_z = psf.dims.n_z
     if volume.shape[2] != n_z:
         raise DimMismatch(f"volume has {volume.shape[2]} depth planes, PSF array has {n_z}")
     dev = f"cuda:{device}"
     H = _to_device_f(psf.data, dev)
     g = _to_device_f(volume.data, dev, np.float64)
-    Hp = hprime_device(H) if _odd(psf.dims.shape) else None
-    return Image._wrap(_to_host_f(forward_project_device(H, g, Hp=Hp)))
+    return Image._wrap(_to_host_f(forward_project_device(H, g)))
 
 
 def backproject_adjoint(psf, image, device: int = 0) -> Volume:
@@ -161,16 +159,12 @@ def backproject_adjoint(psf, image, device: int = 0) -> Volume:
 
 
 def backproject(bp, image, device: int = 0) -> Volume:
-    """projector.py:103-126 on the GPU.  For odd n_s, n_t, H is recovered from
-    H' on the device (the map is an involution) and the voxel-phase gather is
-    used (equal to the H'-stamp form within 1e-12, as the reference's own
-    tests require); even sizes use the H' pixel-stamp gather directly."""
-    from .transform import hprime_device
+    """projector.py:103-126 on the GPU: the H'-stamp sums, run as a polyphase
+    convolution over H' (the pattern of a tap class is the input pixel's
+    phase), for odd and even sizes alike."""
     dev = f"cuda:{device}"
     P = _to_device_f(bp.data, dev)
     f = _to_device_f(image.data, dev, np.float64)
-    if _odd(bp.dims.shape):
-        return Volume._wrap(_to_host_f(backproject_device(hprime_device(P, inverse=True), f, use_hprime=False)))
     return Volume._wrap(_to_host_f(backproject_device(P, f, use_hprime=True)))
 
 
