@@ -2,7 +2,7 @@
 
 Run in the dev container, where the read-only reference is mounted:
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--configs C1,C2,C3,C4] [--small]
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--configs C1,C2,C3,C4] [--small] [--acceptance]
 
 Outputs (committed):
 
@@ -10,6 +10,9 @@ Outputs (committed):
   reference's own test shapes (pkg/tests/test_transform.py, test_oracle.py,
   test_acceptance.py) plus bit-pattern edge cases, each produced by
   ``lfbp.compute_backprojection`` / ``lfbp.compute_psf_from_backprojection``.
+* ``tests/golden/acceptance_suite.json`` -- SHA-256 of the input and of the
+  reference's H' for each of the 50 arrays of the reference's acceptance
+  suite (test_acceptance.py:21-27).
 * ``tests/golden/digests_<C>.json`` -- per-plane SHA-256 of the BASELINE
   workload input (our seeded generator) and of the reference's H' for it.
   Planes are transformed in slabs of ``--slab`` planes; z-planes are
@@ -225,8 +228,41 @@ def make_digests(cfg: str, slab: int):
     print(f"wrote {path}")
 
 
+# the reference's randomized acceptance matrix (test_acceptance.py:21-27):
+# (dims, number of arrays), seeds 1000, 1001, ... in order, density 0.1
+ACCEPTANCE_SUITE = [((9, 9, 3, 3, 3), 20), ((15, 13, 5, 3, 2), 12), ((19, 11, 9, 5, 2), 8),
+                    ((21, 21, 11, 11, 3), 6), ((89, 89, 11, 11, 2), 4)]
+
+
+def make_acceptance(path):
+    """Digests of the reference's H' (and of its inverse) for the 50 arrays of
+    its acceptance suite, drawn by lfbp.random_psf; the tests redraw them with
+    synth.random_psf_like_reference (bit-identical, checked here)."""
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    cases = []
+    seed = 1000
+    for shape, count in ACCEPTANCE_SUITE:
+        for _ in range(count):
+            psf = lfbp.random_psf(Dims5(*shape), density=0.1, seed=seed)
+            mine = random_psf_like_reference(shape, density=0.1, seed=seed)
+            assert psf.data.tobytes(order="F") == mine.tobytes(order="F"), "generator restatement drifted"
+            bp = lfbp.compute_backprojection(psf)
+            inv = lfbp.compute_psf_from_backprojection(bp)
+            assert np.array_equal(inv.data, psf.data)
+            cases.append({"shape": list(shape), "seed": seed, "density": 0.1,
+                          "input_sha256": hashlib.sha256(psf.data.tobytes(order="F")).hexdigest(),
+                          "hprime_sha256": hashlib.sha256(bp.data.tobytes(order="F")).hexdigest()})
+            seed += 1
+    doc = {"source": "lfbp test_acceptance.py:21-27 suite, lfbp.random_psf(density=0.1, seeds 1000..1049), "
+                     "lfbp.compute_backprojection", "cases": cases}
+    with open(path, "w") as f:
+        json.dump(doc, f, indent=1)
+    print(f"wrote {path}: {len(cases)} cases")
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--acceptance", action="store_true")
     ap.add_argument("--small", action="store_true")
     ap.add_argument("--configs", default="")
     ap.add_argument("--slab", type=int, default=8)
@@ -234,6 +270,8 @@ def main():
     if a.small:
         make_small(os.path.join(HERE, "small_cases.npz"))
         make_projector(os.path.join(HERE, "projector_cases.npz"))
+    if a.acceptance:
+        make_acceptance(os.path.join(HERE, "acceptance_suite.json"))
     for c in [c for c in a.configs.split(",") if c]:
         make_digests(c, a.slab)
 

@@ -361,3 +361,43 @@ def test_autotuner_picks_a_candidate_and_stays_exact(monkeypatch):
     n_diff, _ = compare_device(back, src)
     assert n_diff == 0
     torch.cuda.synchronize()
+
+
+def test_acceptance_suite_criteria_1_to_4_on_device():
+    """The reference's acceptance suite (test_acceptance.py:21-27: 50 arrays,
+    density 0.1, seeds 1000..1049) through the device path, criteria 1-4:
+    (1) H' equals the reference's, by digest; (2) the inverse and a second
+    forward pass return H bit for bit; (3) the sorted-order plane sums of H'
+    are the 180-degree rotation of H's, exactly (device reductions); (4) every
+    H'(s', t', :, :, z) slice holds the values of H(mirror s', mirror t', :, :, z)
+    and the sorted per-plane totals agree bitwise."""
+    import hashlib
+    import json
+
+    torch = _torch()
+    from conftest import GOLDEN
+    from paper_2003_09133_b200 import hprime_device
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    from paper_2003_09133_b200.verify import compare_device, rotation_check
+    with open(os.path.join(GOLDEN, "acceptance_suite.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        shape = tuple(c["shape"])
+        H = random_psf_like_reference(shape, density=c["density"], seed=c["seed"])
+        src = to_device(H)
+        hp = hprime_device(src)
+        got = to_host(hp)
+        assert hashlib.sha256(got.tobytes()).hexdigest() == c["hprime_sha256"], c["seed"]       # (1)
+        if shape[0] % 2 and shape[1] % 2:
+            assert compare_device(hprime_device(hp, inverse=True), src)[0] == 0                 # (2)
+            assert compare_device(hprime_device(hp), src)[0] == 0
+        assert rotation_check(src, hp, shape) == 0                                                 # (3)
+        n_s, n_t, n_x, n_y, n_z = shape
+        bp = got.reshape(shape, order="F")
+        flat_bp = bp.reshape(n_s, n_t, n_x * n_y, n_z, order="F")
+        flat_h = H[::-1, ::-1].reshape(n_s, n_t, n_x * n_y, n_z, order="F")
+        assert np.array_equal(np.sort(flat_bp, axis=2), np.sort(flat_h, axis=2))                   # (4)
+        for z in range(n_z):
+            assert np.sort(H[..., z], axis=None).sum(dtype=np.float64) == \
+                np.sort(bp[..., z], axis=None).sum(dtype=np.float64)
+    torch.cuda.synchronize()

@@ -162,3 +162,27 @@ def test_pairwise_order_long_slices():
         v = np.sort(rng.random(k).astype(np.float32) * rng.random(k).astype(np.float32) ** 7)
         want = v.reshape(1, 1, k).sum(axis=-1, dtype=np.float64)[0, 0]
         assert pairwise_sum(v) == want, k
+
+
+def _acceptance_cases():
+    import json
+    import os
+
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "acceptance_suite.json")) as f:
+        return json.load(f)["cases"]
+
+
+def test_oracle_matches_reference_acceptance_suite():
+    """The reference's 50-array acceptance matrix (test_acceptance.py:21-27,
+    criterion 1): our redraw of lfbp.random_psf is bit-identical to the
+    reference's input and the oracle reproduces the reference's H' for every
+    array (digests produced by the reference, tests/golden/make_golden.py)."""
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    cases = _acceptance_cases()
+    assert len(cases) == 50
+    for c in cases:
+        H = random_psf_like_reference(tuple(c["shape"]), density=c["density"], seed=c["seed"])
+        assert hashlib.sha256(H.tobytes(order="F")).hexdigest() == c["input_sha256"]
+        Hp = hprime_oracle(H)
+        assert hashlib.sha256(np.asfortranarray(Hp).tobytes(order="F")).hexdigest() == c["hprime_sha256"], c["seed"]
