@@ -319,7 +319,7 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
   // judged at its steady-state rate, not on one launch after an idle gap);
   // score = median over rounds of the per-launch time
   constexpr int kCand = kNumCandidates;
-  constexpr int kRounds = 3;
+  constexpr int kRounds = 4;
   const Knobs* cand = key.cls == 1 ? kCandidates : kSmallCandidates;
   const int n_cand = key.cls == 1 ? kNumCandidates : kNumSmallCandidates;
   HpPlan plans[kCand];
@@ -362,15 +362,23 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
       t[c][r] /= float(reps);
     }
   }
+  // round 0 is a warm-up (the first window after switching plans can read
+  // several % off either way); score = median of the other rounds
   float best_ms = 1e30f;
   bool found = false;
+  const bool log = env_int("LFBP_TUNE_LOG", 0) != 0;
   for (int c = 0; c < n_cand; ++c) {
     if (!ok[c]) continue;
-    float v[kRounds];
-    for (int r = 0; r < kRounds; ++r) v[r] = t[c][r];
-    std::sort(v, v + kRounds);
-    if (v[kRounds / 2] < best_ms) {
-      best_ms = v[kRounds / 2];
+    float v[kRounds - 1];
+    for (int r = 1; r < kRounds; ++r) v[r - 1] = t[c][r];
+    std::sort(v, v + kRounds - 1);
+    const float med = v[(kRounds - 1) / 2];
+    if (log)
+      fprintf(stderr, "[lfbp tune] (%lld,%lld,%lld,%lld) E=%d class=%d knobs {%d,%d,%d,%d}: %.4f ms\n",
+              (long long)key.n_s, (long long)key.n_t, (long long)key.n_x, (long long)key.n_y, key.E, key.cls,
+              cand[c].stages, cand[c].stage_kb, cand[c].cwarps, cand[c].subwarp, med);
+    if (med < best_ms) {
+      best_ms = med;
       best = cand[c];
       found = true;
     }

@@ -1,6 +1,6 @@
 #!/bin/bash
 # refresh the committed evidence: bench lines, K1 launch list, one full ncu
-# capture of the tuned K1 on C2.  The ncu runs pin the plan the plain run's
+# capture of the tuned K1 on C2.  The ncu runs pin the plan the headline bench run's
 # autotuner chose (env knobs), so no autotuning happens under the profiler
 # and the first timed launch is launch index = warmup.
 mkdir -p gpurun_out
@@ -11,7 +11,7 @@ done
 CMD="python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --no-verify"
 $CMD > gpurun_out/plain_launch.log 2>&1; echo plain_rc=$?
 KN=$(python -c "
-import json; d=json.loads([l for l in open('gpurun_out/plain_launch.log') if l.startswith('{')][-1])
+import json; d=json.loads([l for l in open("gpurun_out/bench.log") if l.startswith("{")][-1])
 k=d['config']['kernel_plan']['knobs']; print(f'LFBP_STAGES={k[0]} LFBP_STAGE_KB={k[1]} LFBP_CONSUMER_WARPS={k[2]} LFBP_SUBWARP={k[3]}')")
 echo "pinned plan: $KN" | tee gpurun_out/ncu_plan.txt
 env $KN $CMD > gpurun_out/plain_pinned.log 2>&1 && env $KN ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo ncu1_rc=$?

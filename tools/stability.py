@@ -1,5 +1,6 @@
 """Run-to-run stability of K1 plans: interleaved repeats of a few plans.
     python tools/stability.py --config C2 --plans "3,48,16,16;4,48,16,16;3,48,8,8" --rounds 5 --reps 200
+A plan is stages,stage_kb,consumer_warps,sub_width[,kflags (LFBP_KFLAGS)].
 """
 import argparse
 import json
@@ -26,12 +27,12 @@ def main():
     src = f_order_empty(w.shape, tdt)
     src.permute(4, 3, 2, 1, 0).reshape(-1).uniform_()
     out = f_order_empty(w.shape, tdt)
-    keys = ("LFBP_STAGES", "LFBP_STAGE_KB", "LFBP_CONSUMER_WARPS", "LFBP_SUBWARP")
+    keys = ("LFBP_STAGES", "LFBP_STAGE_KB", "LFBP_CONSUMER_WARPS", "LFBP_SUBWARP", "LFBP_KFLAGS")
     plans = [tuple(int(v) for v in p.split(",")) for p in a.plans.split(";")]
     res = {p: [] for p in plans}
     for r in range(a.rounds):
         for pl in plans:
-            for k, v in zip(keys, pl):
+            for k, v in zip(keys, list(pl) + [""] * len(keys)):
                 os.environ[k] = str(v)
             for _ in range(5):
                 hprime_device(src, out=out)
