@@ -46,6 +46,8 @@ def rearrange_multi_host(src: np.ndarray, dst: np.ndarray, devices, inverse: boo
         raise ValueError("src and dst must match")
     if not (src.flags.f_contiguous and dst.flags.f_contiguous):
         raise ValueError("arrays must be F-contiguous")
+    if np.shares_memory(src, dst):
+        raise ValueError("src and dst overlap (the rearrangement is not in place; transform.py:113-135 returns a new array)")
     devs = (ctypes.c_int * len(devices))(*devices)
     rc = _native.lib().lfbp_hprime_multi(src.ctypes.data_as(ctypes.c_void_p), dst.ctypes.data_as(ctypes.c_void_p),
                                          _native.dims_array(src.shape), code, int(inverse), len(devices), devs,

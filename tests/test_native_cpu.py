@@ -146,3 +146,10 @@ def test_dropin_mirrors_reference_errors_and_types():
     # the even-dims inverse is refused before any device work
     with pytest.raises(EvenPixelDims):
         compute_psf_from_backprojection(BackprojArray._wrap(Dims5(4, 5, 3, 3, 1), np.ones((4, 5, 3, 3, 1), order="F")))
+
+
+def test_multi_host_rejects_overlapping_buffers():
+    from paper_2003_09133_b200.shard import rearrange_multi_host
+    H = np.zeros((5, 5, 3, 3, 2), dtype=np.float32, order="F")
+    with pytest.raises(ValueError, match="overlap"):
+        rearrange_multi_host(H, H, [0])
