@@ -182,6 +182,16 @@ int lfbp_rl_update_device(double* g, const double* back, const double* norm, int
  * B200 defaults (148 SMs, 227 KB smem/CTA) when no GPU is present. */
 int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len);
 
+/* Page-locked host blocks for result arrays (the drop-ins' fresh H' / H,
+ * reference transform.py:126 / 153 allocate them with np.zeros / np.empty):
+ * D2H lands in them at full PCIe speed with no staging copy.  Freed blocks
+ * stay cached for reuse (pinning is the expensive part, ~0.5 s per GB) up
+ * to LFBP_PIN_CACHE_MB (default 16384) bytes; lfbp_host_cache_release
+ * returns the cached blocks to the system. */
+int lfbp_host_alloc(int64_t bytes, void** out);
+int lfbp_host_free(void* p);
+int lfbp_host_cache_release(void);
+
 /* Kernel launches issued by this library since load (all entry points). */
 int64_t lfbp_launch_count(void);
 

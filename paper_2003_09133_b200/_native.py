@@ -27,7 +27,8 @@ EXPORTS = (
     "lfbp_lf5_read_header", "lfbp_lf5_create", "lfbp_lf5_transform_file", "lfbp_lf5_load_device",
     "lfbp_lf5_store_device", "lfbp_forward_project_device", "lfbp_backproject_device",
     "lfbp_safe_divide_device", "lfbp_forward_project2_device", "lfbp_max_device",
-    "lfbp_safe_divide_peak_device", "lfbp_rl_update_device",
+    "lfbp_safe_divide_peak_device", "lfbp_rl_update_device", "lfbp_host_alloc", "lfbp_host_free",
+    "lfbp_host_cache_release",
 )
 
 _lock = threading.Lock()
@@ -73,6 +74,9 @@ _SIGS = {
                                                     ctypes.c_void_p]),
     "lfbp_rl_update_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                              ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p]),
+    "lfbp_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "lfbp_host_free": (ctypes.c_int, [ctypes.c_void_p]),
+    "lfbp_host_cache_release": (ctypes.c_int, []),
     "lfbp_launch_count": (ctypes.c_int64, []),
     "lfbp_last_error": (ctypes.c_char_p, []),
     "lfbp_version": (ctypes.c_char_p, []),

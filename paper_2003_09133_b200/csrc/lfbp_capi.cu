@@ -590,6 +590,78 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
 
 #include "projector_capi.inc"
 
+// ---- pinned host blocks with a size-matched free cache ----
+namespace {
+std::mutex g_pin_mu;
+std::map<void*, int64_t> g_pin_live;            // block -> capacity
+std::multimap<int64_t, void*> g_pin_cache;      // capacity -> free block
+int64_t g_pin_cached = 0;
+}  // namespace
+
+int lfbp_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(LFBP_ERR_ARGUMENT, "bad host_alloc arguments");
+  *out = nullptr;
+  const int64_t want = std::max<int64_t>(bytes, 1);
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    // smallest cached block that fits and wastes at most a quarter of it
+    auto it = g_pin_cache.lower_bound(want);
+    if (it != g_pin_cache.end() && it->first - want <= it->first / 4) {
+      *out = it->second;
+      g_pin_live[it->second] = it->first;
+      g_pin_cached -= it->first;
+      g_pin_cache.erase(it);
+      return LFBP_OK;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, size_t(want), cudaHostAllocPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LFBP_ERR_CUDA, "cudaHostAlloc(%lld): %s", (long long)want, cudaGetErrorString(e));
+  }
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_live[p] = want;
+  *out = p;
+  return LFBP_OK;
+}
+
+int lfbp_host_free(void* p) {
+  if (!p) return LFBP_OK;
+  int64_t cap;
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_live.find(p);
+    if (it == g_pin_live.end()) return fail(LFBP_ERR_ARGUMENT, "pointer was not allocated by lfbp_host_alloc");
+    cap = it->second;
+    g_pin_live.erase(it);
+    const int64_t limit = int64_t(env_int("LFBP_PIN_CACHE_MB", 16384)) << 20;
+    if (g_pin_cached + cap <= limit) {
+      g_pin_cache.emplace(cap, p);
+      g_pin_cached += cap;
+      return LFBP_OK;
+    }
+  }
+  cudaError_t e = cudaFreeHost(p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LFBP_ERR_CUDA, "cudaFreeHost: %s", cudaGetErrorString(e));
+  }
+  return LFBP_OK;
+}
+
+int lfbp_host_cache_release(void) {
+  std::multimap<int64_t, void*> blocks;
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    blocks.swap(g_pin_cache);
+    g_pin_cached = 0;
+  }
+  for (auto& kv : blocks) cudaFreeHost(kv.second);
+  cudaGetLastError();
+  return LFBP_OK;
+}
+
 int64_t lfbp_launch_count(void) { return g_launches.load(); }
 
 const char* lfbp_last_error(void) { return g_err.c_str(); }

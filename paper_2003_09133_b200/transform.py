@@ -74,14 +74,40 @@ def _host_flags() -> int:
     return {"stage": _native.HOST_STAGE, "register": _native.HOST_REGISTER, "driver": 0}.get(mode, _native.HOST_STAGE)
 
 
+def _out_pinned() -> bool:
+    """Where the drop-in's fresh result array lives (LFBP_OUT_MODE): "pinned"
+    (default: a page-locked block from the library's cached host allocator,
+    so the D2H lands directly) or "pageable" (plain numpy; the D2H is staged
+    through the pipeline's pinned chunks)."""
+    return os.environ.get("LFBP_OUT_MODE", "pinned") == "pinned"
+
+
+class _PinnedBlock:
+    """Owner of one ``lfbp_host_alloc`` block, exposed to numpy through the
+    array interface: the ndarray keeps it alive, and the block goes back to
+    the library's cache when the last array on it is gone."""
+
+    ptr = None
+
+    def __init__(self, nbytes: int):
+        ptr = ctypes.c_void_p()
+        _native.check(_native.lib().lfbp_host_alloc(nbytes, ctypes.byref(ptr)))
+        self.ptr = ptr.value
+        self.nbytes = nbytes
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        lib = _native._lib
+        if lib is not None and self.ptr:
+            lib.lfbp_host_free(ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+
 def _pinned_empty(shape, dtype) -> np.ndarray:
-    """F-ordered host array in page-locked memory (torch's caching host
-    allocator), so the D2H leg runs at full PCIe speed."""
-    import torch
+    """F-ordered host array in page-locked memory (no torch involved)."""
     n = int(np.prod(shape)) * np.dtype(dtype).itemsize
-    buf = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)
-    flat = buf.numpy()[:n].view(dtype)
-    return flat.reshape(shape, order="F")
+    raw = np.asarray(_PinnedBlock(max(n, 1)))
+    return raw[:n].view(dtype).reshape(shape, order="F")
 
 
 def _rearrange_host(data: np.ndarray, dims, inverse: bool, errs, device: int = 0) -> np.ndarray:
@@ -99,7 +125,7 @@ def _rearrange_host(data: np.ndarray, dims, inverse: bool, errs, device: int = 0
     if inverse and (shape[0] % 2 == 0 or shape[1] % 2 == 0):
         raise even(f"inverse undefined for even pixel dims (n_s, n_t)=({shape[0]}, {shape[1]}): "
                    "the forward mapping drops elements")
-    out = _pinned_empty(shape, src.dtype)
+    out = _pinned_empty(shape, src.dtype) if _out_pinned() else np.empty(shape, dtype=src.dtype, order="F")
     rc = _native.lib().lfbp_hprime_host(src.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p),
                                         dvec, code, int(inverse), int(device), _host_flags())
     _native.check(rc, invalid, even)

@@ -432,3 +432,30 @@ def test_criterion_7_speed_through_the_dropin():
     compute_backprojection(psf2)
     t_big, _ = best(lambda: compute_backprojection(psf2))
     assert t_big < 5.0
+
+
+@pytest.mark.gpu
+def test_pinned_result_blocks_are_cached_and_outlive_their_owner():
+    """The drop-ins' result arrays live in page-locked blocks of the library's
+    cached host allocator (no torch): freed blocks are reused, and a result
+    stays valid for as long as an array refers to it."""
+    import ctypes
+    import gc
+
+    from paper_2003_09133_b200 import _native
+    lib = _native.lib()
+    a, b = ctypes.c_void_p(), ctypes.c_void_p()
+    assert lib.lfbp_host_alloc(1 << 20, ctypes.byref(a)) == 0
+    assert lib.lfbp_host_free(a) == 0
+    assert lib.lfbp_host_alloc((1 << 20) - 4096, ctypes.byref(b)) == 0   # fits the cached block
+    assert b.value == a.value
+    assert lib.lfbp_host_free(b) == 0
+    assert lib.lfbp_host_free(ctypes.c_void_p(12345)) != 0                 # not ours: refused
+    from paper_2003_09133_b200 import Dims5, PsfArray, compute_backprojection
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    H = random_psf_like_reference((21, 19, 7, 5, 3), density=0.9, seed=11, dtype=np.float32)
+    want = fbytes(hprime_oracle(H))
+    data = compute_backprojection(PsfArray._wrap(Dims5(*H.shape), H)).data
+    gc.collect()
+    assert data.tobytes(order="F") == want
+    assert lib.lfbp_host_cache_release() == 0

@@ -25,6 +25,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--dropin-only", action="store_true", help="skip the PCIe and C-ABI legs")
+    ap.add_argument("--modes", default="stage,register,driver")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -74,13 +76,15 @@ def main():
             pin_out.copy_(dev_b, non_blocking=True)
         s1.synchronize()
         s2.synchronize()
-    for name, fn, nb in (("h2d", h2d, w.nbytes), ("d2h", d2h, w.nbytes), ("h2d+d2h", both, 2 * w.nbytes)):
+    legs = () if a.dropin_only else (("h2d", h2d, w.nbytes), ("d2h", d2h, w.nbytes), ("h2d+d2h", both, 2 * w.nbytes))
+    for name, fn, nb in legs:
         best, med = timed(fn)
         print(json.dumps({"path": "pcie " + name, "best_ms": round(best * 1e3, 2), "GBps": round(nb / best / 1e9, 2)}),
               flush=True)
     del dev_a, dev_b
     ref = None
-    for mb in (34, 70):
+    chunk_env = os.environ.get("LFBP_CHUNK_MB")
+    for mb in ((70,) if a.dropin_only else (34, 70)):
         os.environ["LFBP_CHUNK_MB"] = str(mb)
 
         def call():
@@ -93,10 +97,12 @@ def main():
                           "med_ms": round(med * 1e3, 2), "GBps_rw": round(step_bytes / best / 1e9, 2),
                           "same": dig == ref}), flush=True)
     os.environ.pop("LFBP_CHUNK_MB", None)
+    if chunk_env:
+        os.environ["LFBP_CHUNK_MB"] = chunk_env
     pageable = np.array(H, order="F")
     pageable.flags.writeable = False
     psf = PsfArray._wrap(Dims5(*w.shape), pageable)
-    for reg in ("stage", "register", "driver"):
+    for reg in a.modes.split(","):
         os.environ["LFBP_HOST_MODE"] = reg
         out = {}
 
@@ -104,7 +110,9 @@ def main():
             out["bp"] = compute_backprojection(psf)
         best, med = timed(dropin)
         dig = hashlib.sha256(out["bp"].data.tobytes(order="F")).hexdigest()
-        print(json.dumps({"path": "drop-in pageable input", "host_mode": reg, "best_ms": round(best * 1e3, 2),
+        print(json.dumps({"path": "drop-in pageable input", "host_mode": reg,
+                          "copy_threads": os.environ.get("LFBP_COPY_THREADS", "default"),
+                          "chunk_mb": os.environ.get("LFBP_CHUNK_MB", "64"), "best_ms": round(best * 1e3, 2),
                           "med_ms": round(med * 1e3, 2), "GBps_rw": round(step_bytes / best / 1e9, 2),
                           "same": dig == ref}), flush=True)
 
