@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--psf", default="C1")
     ap.add_argument("--image", type=int, default=256)
     ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--quick", action="store_true", help="forward (H') and H'-backprojection only")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -49,6 +50,13 @@ def main():
     t_fwd_h = timed(lambda: forward_project_device(H, g))
     t_fwd = timed(lambda: forward_project_device(H, g, Hp=Hp))
     t_bp = timed(lambda: backproject_device(Hp, f))
+    if a.quick:
+        print(json.dumps({"psf": w.name, "image": N, "rl": os.environ.get("LFBP_PROJ_RL", ""),
+                          "tk": os.environ.get("LFBP_PROJ_TK", ""), "forward_ms": round(t_fwd, 3),
+                          "backproject_ms": round(t_bp, 3),
+                          "forward_fp64_tflops": round(2 * float(N) * N * n_s * n_t * n_z / (t_fwd * 1e-3) / 1e12, 3),
+                          "backproject_fp64_tflops": round(2 * float(N) * N * n_s * n_t * n_z / (t_bp * 1e-3) / 1e12, 3)}))
+        return
     t_adj = timed(lambda: backproject_device(H, f, use_hprime=False))
     norm = backproject_device(Hp, torch.ones((N, N), dtype=torch.float64, device="cuda").t().contiguous().t())
     scratch = torch.empty(1, dtype=torch.float64, device="cuda")
