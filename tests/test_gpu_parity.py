@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import load_digests
+from conftest import ROOT, load_digests
 from oracle.hprime_oracle import hprime_oracle
 
 pytestmark = pytest.mark.gpu
@@ -459,3 +459,16 @@ def test_pinned_result_blocks_are_cached_and_outlive_their_owner():
     gc.collect()
     assert data.tobytes(order="F") == want
     assert lib.lfbp_host_cache_release() == 0
+
+
+@pytest.mark.gpu
+def test_randomised_shapes_plans_and_z_ranges():
+    """tools/fuzz_parity.py: random valid shapes (odd / even, n_x = 1..21),
+    f32 / f64 raw bit patterns (NaN payloads, denormals, -0.0), forward and
+    inverse, random plan knobs and z sub-ranges; every case bit-exact and
+    the planes outside the range untouched."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("fuzz_parity", os.path.join(ROOT, "tools", "fuzz_parity.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    assert mod.run(60, seed=2024, verbose=False) == []
