@@ -472,3 +472,20 @@ def test_randomised_shapes_plans_and_z_ranges():
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     assert mod.run(60, seed=2024, verbose=False) == []
+
+
+@pytest.mark.gpu
+def test_plain_c_client_round_trip(tmp_path):
+    """examples/hprime_host.c: the host path driven from C (forward, inverse,
+    bit-exact round trip, single-element KAT)."""
+    import subprocess
+    sys_path_root = ROOT
+    exe = str(tmp_path / "hprime_host")
+    libdir = os.path.join(sys_path_root, "paper_2003_09133_b200")
+    r = subprocess.run(["gcc", "-std=c99", "-O2", "-I", os.path.join(sys_path_root, "include"),
+                        os.path.join(sys_path_root, "examples", "hprime_host.c"), "-L", libdir, "-lhprime",
+                        f"-Wl,-rpath,{libdir}", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "round trip and single-element KAT ok" in r.stdout

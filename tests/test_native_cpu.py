@@ -153,3 +153,23 @@ def test_multi_host_rejects_overlapping_buffers():
     H = np.zeros((5, 5, 3, 3, 2), dtype=np.float32, order="F")
     with pytest.raises(ValueError, match="overlap"):
         rearrange_multi_host(H, H, [0])
+
+
+def _build_c_example(tmp_path):
+    """examples/hprime_host.c against include/lfbp_hprime.h as plain C99."""
+    import subprocess
+    from conftest import ROOT
+    exe = str(tmp_path / "hprime_host")
+    libdir = os.path.join(ROOT, "paper_2003_09133_b200")
+    r = subprocess.run(["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "hprime_host.c"), "-L", libdir, "-lhprime",
+                        f"-Wl,-rpath,{libdir}", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_header_is_plain_c_and_the_abi_runs_from_c(tmp_path):
+    import subprocess
+    r = subprocess.run([_build_c_example(tmp_path), "--abi"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "abi ok" in r.stdout
