@@ -151,11 +151,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return pol;
 }
 
-// Producer warp: stage the n_x source runs of unit `u` into `stage`, one
-// run per lane (x = lane, lane + 32, ...), completion on `bar`.
+// Producer warp `pw` of p.producers: stage its share of the n_x source runs
+// of unit `u` into `stage`, one run per lane (x = 32 pw + lane, then
+// + 32 producers, ...), completion on `bar` (one expect_tx arrive per
+// producer warp).  The bulk copies take uniform operands, so ptxas issues a
+// warp's runs one lane at a time; several producer warps issue in parallel.
 template <int E>
 __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __restrict__ src, uint32_t u,
-                                           uint8_t* stage, uint32_t bar, int lane, uint64_t policy) {
+                                           uint8_t* stage, uint32_t bar, int lane, int pw, uint64_t policy) {
   using T = typename Word<E>::T;
   const Unit w = decode_unit(p, u);
   const int64_t run_bytes = w.run_elems * E;
@@ -164,7 +167,7 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
   const int64_t b0 = w.run_off0 * E;
   uint32_t tx = 0;
   if (run_bytes > 0) {
-    for (int32_t x = lane; x < p.n_x; x += 32) {
+    for (int32_t x = 32 * pw + lane; x < p.n_x; x += 32 * p.producers) {
       const int64_t b = b0 + x * xstride;
       const int64_t a_lo = b & ~int64_t(15);
       int64_t a_hi = (b + run_bytes + 15) & ~int64_t(15);
@@ -185,7 +188,7 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
         *reinterpret_cast<T*>(dst + (q - a_lo)) = *reinterpret_cast<const T*>(src + q);
     }
   }
-  if (lane == 0) {
+  if (lane == 0 && pw == 0) {
     UnitHdr* h = reinterpret_cast<UnitHdr*>(stage);
     h->plane_off = w.z * (p.n_s * p.n_t * p.n_x * p.n_y);
     h->y = static_cast<int32_t>(w.y);
@@ -386,8 +389,8 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
   }
 }
 
-// Warp 0 (one elected lane) produces, warps 1.. consume; full/empty mbarrier
-// ring of `stages` buffers, so consumer warps never wait for each other.
+// Warps 0..producers-1 produce, the rest consume; full/empty mbarrier ring
+// of `stages` buffers, so consumer warps never wait for each other.
 template <int E>
 __global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8_t* __restrict__ src,
                                                      uint8_t* __restrict__ dst) {
@@ -401,16 +404,17 @@ __global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8
   const uint32_t mine = (n_units - first + stride - 1) / stride;
   const int S = p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nc = (blockDim.x >> 5) - 1;
+  const int np = p.producers;
+  const int nc = (blockDim.x >> 5) - np;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&full[s]), np);
       mbar_init(smem_u32(&empty[s]), nc);
     }
     fence_barrier_init();
   }
   __syncthreads();
-  if (warp == 0) {
+  if (warp < np) {
     const uint64_t policy = policy_evict_first();
     int st = 0;
     uint32_t ph = 0;
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8
         fence_proxy_async_smem();
       }
       issue_unit<E>(p, src, first + k * stride, stages + static_cast<int64_t>(st) * p.stage_bytes,
-                    smem_u32(&full[st]), lane, policy);
+                    smem_u32(&full[st]), lane, warp, policy);
       if (++st == S) {
         st = 0;
         ph ^= 1u;
@@ -434,7 +438,7 @@ __global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8
   for (uint32_t k = 0; k < mine; ++k) {
     mbar_wait(smem_u32(&full[st]), ph);
     consume_unit<E>(p, dst, stages + static_cast<int64_t>(st) * p.stage_bytes,
-                    stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - 1, nc, lane);
+                    stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - np, nc, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     if (++st == S) {

@@ -91,6 +91,7 @@ struct HpPlan {
   int32_t flags;              // HP_FLAG_*
   int32_t sub_width;          // lanes per output row (2, 4, 8, 16 or 32)
   int32_t gx_inc;             // (sub_width * 16/elem) mod n_x: phase advance of one stride
+  int32_t producers;          // producer warps (warps 0..producers-1); they split a unit's n_x runs
   int64_t n_units;            // z_count * n_chunks * n_bands * n_y  (< 2^31)
   HpFastDiv nx_div;           // mod n_x on the element path
   HpFastDiv ny_div;           // unit decode / y' wrap

@@ -217,7 +217,12 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   int cwarps = env_int("LFBP_CONSUMER_WARPS", kn.cwarps);
   if (cwarps <= 0) cwarps = 12;
   cwarps = std::max(1, std::min(16, cwarps));
-  const int threads = 32 * (1 + cwarps);  // producer + consumers
+  // producer warps: one per 32 runs of a unit (the runs of one warp issue
+  // serially), within the kernel's 17-warp launch bound
+  int prod = env_int("LFBP_PRODUCERS", int((d[2] + 31) / 32));
+  prod = std::max(1, std::min(prod, 17 - cwarps));
+  p.producers = prod;
+  const int threads = 32 * (prod + cwarps);  // producers + consumers
   p.threads = threads;
 
   const int64_t units = z_count * p.n_chunks * int64_t(p.n_bands) * d[3];
@@ -576,10 +581,10 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
                    "{\"elem\": %d, \"J\": %d, \"n_bands\": %d, \"C\": %d, \"n_chunks\": %d, \"row_pitch\": %d, "
                    "\"stage_bytes\": %d, \"stages\": %d, \"threads\": %d, \"smem_bytes\": %d, \"ctas_per_sm\": %d, "
                    "\"grid\": %d, \"n_units\": %lld, \"sub_width\": %d, \"sm_count\": %d, \"device_props\": \"%s\", "
-                   "\"autotuned\": %s, \"knobs\": [%d, %d, %d, %d]}",
+                   "\"producers\": %d, \"autotuned\": %s, \"knobs\": [%d, %d, %d, %d]}",
                    p.elem, p.J, p.n_bands, p.C, p.n_chunks, p.row_pitch, p.stage_bytes, p.stages, p.threads,
                    p.smem_bytes, p.ctas_per_sm, p.grid, (long long)p.n_units, p.sub_width, dp.sm_count,
-                   dp.real ? "queried" : "b200-defaults", tuned ? "true" : "false",
+                   dp.real ? "queried" : "b200-defaults", p.producers, tuned ? "true" : "false",
                    env_int("LFBP_STAGES", kn.stages), env_int("LFBP_STAGE_KB", kn.stage_kb),
                    env_int("LFBP_CONSUMER_WARPS", kn.cwarps), env_int("LFBP_SUBWARP", kn.subwarp));
   if (w < 0 || w >= buf_len) return fail(LFBP_ERR_ARGUMENT, "buffer too small");

@@ -154,9 +154,12 @@ def test_random_shapes_match_oracle(shape, dtype):
     {"LFBP_SUBWARP": "2"}, {"LFBP_SUBWARP": "4"}, {"LFBP_SUBWARP": "8"}, {"LFBP_SUBWARP": "32"},
     {"LFBP_SUBWARP": "16", "LFBP_CONSUMER_WARPS": "3"}, {"LFBP_SUBWARP": "4", "LFBP_STAGE_MAX_KB": "2"},
     {"LFBP_SUBWARP": "8", "LFBP_STAGE_MAX_KB": "2", "LFBP_STAGES": "2"},
+    # several producer warps splitting a unit's runs (one warp has none when n_x <= 32)
+    {"LFBP_PRODUCERS": "2"}, {"LFBP_PRODUCERS": "3", "LFBP_STAGE_MAX_KB": "2"},
+    {"LFBP_PRODUCERS": "4", "LFBP_CONSUMER_WARPS": "13", "LFBP_SUBWARP": "4"},
 ])
 @pytest.mark.parametrize("shape,dtype", [((55, 55, 11, 11, 2), np.float32), ((27, 20, 13, 5, 2), np.float64),
-                                         ((66, 41, 21, 9, 1), np.float32)])
+                                         ((66, 41, 21, 9, 1), np.float32), ((81, 12, 41, 3, 2), np.float32)])
 def test_plan_variants_are_bit_exact(monkeypatch, env, shape, dtype):
     torch = _torch()
     from paper_2003_09133_b200 import hprime_device, plan
@@ -166,6 +169,8 @@ def test_plan_variants_are_bit_exact(monkeypatch, env, shape, dtype):
     p = plan(shape, dtype)
     if env.get("LFBP_STAGE_MAX_KB") == "2":
         assert p["n_chunks"] > 1
+    if "LFBP_PRODUCERS" in env:
+        assert p["producers"] == int(env["LFBP_PRODUCERS"])
     H = random_psf_like_reference(shape, density=0.9, seed=7, dtype=dtype)
     out = hprime_device(to_device(H))
     torch.cuda.synchronize()
