@@ -106,10 +106,14 @@ __device__ __forceinline__ Unit decode_unit(const HpPlan& p, uint32_t u) {
     r2 = hp_div(p.ny_div, r);
     w.y = r - r2 * p.ny_div.d;
   } else {  // consecutive units: neighbouring y (their output rows interleave in L2)
-    const uint32_t r = hp_div(p.ny_div, u);
-    w.y = u - r * p.ny_div.d;
-    r2 = hp_div(p.nb_div, r);
-    band = static_cast<int32_t>(r - r2 * p.nb_div.d);
+    r2 = hp_div(p.zc_div, u);
+    const uint32_t r = u - r2 * p.zc_div.d;
+    const uint32_t yb = hp_div(p.yblk_div, r);
+    const uint32_t rem = r - yb * p.yblk_div.d;
+    const HpFastDiv& tdiv = (static_cast<int32_t>(yb) == p.n_yblocks - 1) ? p.tyl_div : p.ty_div;
+    const uint32_t b = hp_div(tdiv, rem);
+    band = static_cast<int32_t>(b);
+    w.y = yb * p.ty_div.d + (rem - b * tdiv.d);
   }
   uint32_t r3 = hp_div(p.nc_div, r2);
   const int32_t chunk = static_cast<int32_t>(r2 - r3 * p.nc_div.d);

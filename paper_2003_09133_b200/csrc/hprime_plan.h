@@ -97,6 +97,13 @@ struct HpPlan {
   HpFastDiv ny_div;           // unit decode / y' wrap
   HpFastDiv nb_div;           // unit decode: bands
   HpFastDiv nc_div;           // unit decode: chunks
+  // unit order inside one (z, chunk): y in blocks of tile_y, y fastest within
+  // a block, then band; the last block holds the remaining y (tile_y = n_y:
+  // plain y-fastest order)
+  int32_t tile_y, n_yblocks;
+  HpFastDiv zc_div;           // n_y * n_bands: units per (z, chunk)
+  HpFastDiv yblk_div;         // tile_y * n_bands: units per full y block
+  HpFastDiv ty_div, tyl_div;  // tile_y, and the last block's y count
 };
 
 // Valid Dims5 (reference arrays.py:53-67): all >= 1, n_x and n_y odd,

@@ -254,6 +254,20 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   p.ny_div = hp_fastdiv_make(static_cast<uint32_t>(d[3]));
   p.nb_div = hp_fastdiv_make(static_cast<uint32_t>(p.n_bands));
   p.nc_div = hp_fastdiv_make(static_cast<uint32_t>(p.n_chunks));
+  // y blocks of 4 when a unit has more than 32 source runs: concurrent units
+  // then span 4 y x ~37 bands instead of all y x ~3 bands, so both the runs
+  // they read and the rows they write sit in longer contiguous stretches
+  // ((181,181,95,55): 0.74 -> 0.82 of copy; (307,307,51,51): 0.84 -> 0.86).
+  // With n_x <= 32 (all BASELINE configs) plain y-fastest order measured best
+  // (profiles/r01_order_probe.jsonl).
+  int ty = env_int("LFBP_TILE_Y", d[2] > 32 ? 4 : int(d[3]));
+  ty = std::max<int>(1, std::min<int>(ty, int(d[3])));
+  p.tile_y = ty;
+  p.n_yblocks = static_cast<int32_t>((d[3] + ty - 1) / ty);
+  p.zc_div = hp_fastdiv_make(static_cast<uint32_t>(d[3] * p.n_bands));
+  p.yblk_div = hp_fastdiv_make(static_cast<uint32_t>(int64_t(ty) * p.n_bands));
+  p.ty_div = hp_fastdiv_make(static_cast<uint32_t>(ty));
+  p.tyl_div = hp_fastdiv_make(static_cast<uint32_t>(d[3] - int64_t(ty) * (p.n_yblocks - 1)));
   return LFBP_OK;
 }
 
@@ -581,10 +595,10 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
                    "{\"elem\": %d, \"J\": %d, \"n_bands\": %d, \"C\": %d, \"n_chunks\": %d, \"row_pitch\": %d, "
                    "\"stage_bytes\": %d, \"stages\": %d, \"threads\": %d, \"smem_bytes\": %d, \"ctas_per_sm\": %d, "
                    "\"grid\": %d, \"n_units\": %lld, \"sub_width\": %d, \"sm_count\": %d, \"device_props\": \"%s\", "
-                   "\"producers\": %d, \"autotuned\": %s, \"knobs\": [%d, %d, %d, %d]}",
+                   "\"producers\": %d, \"tile_y\": %d, \"autotuned\": %s, \"knobs\": [%d, %d, %d, %d]}",
                    p.elem, p.J, p.n_bands, p.C, p.n_chunks, p.row_pitch, p.stage_bytes, p.stages, p.threads,
                    p.smem_bytes, p.ctas_per_sm, p.grid, (long long)p.n_units, p.sub_width, dp.sm_count,
-                   dp.real ? "queried" : "b200-defaults", p.producers, tuned ? "true" : "false",
+                   dp.real ? "queried" : "b200-defaults", p.producers, p.tile_y, tuned ? "true" : "false",
                    env_int("LFBP_STAGES", kn.stages), env_int("LFBP_STAGE_KB", kn.stage_kb),
                    env_int("LFBP_CONSUMER_WARPS", kn.cwarps), env_int("LFBP_SUBWARP", kn.subwarp));
   if (w < 0 || w >= buf_len) return fail(LFBP_ERR_ARGUMENT, "buffer too small");

@@ -157,6 +157,9 @@ def test_random_shapes_match_oracle(shape, dtype):
     # several producer warps splitting a unit's runs (one warp has none when n_x <= 32)
     {"LFBP_PRODUCERS": "2"}, {"LFBP_PRODUCERS": "3", "LFBP_STAGE_MAX_KB": "2"},
     {"LFBP_PRODUCERS": "4", "LFBP_CONSUMER_WARPS": "13", "LFBP_SUBWARP": "4"},
+    # unit order in y blocks (ragged last block), alone and with i-chunks / bands
+    {"LFBP_TILE_Y": "1"}, {"LFBP_TILE_Y": "3"}, {"LFBP_TILE_Y": "2", "LFBP_STAGE_MAX_KB": "2"},
+    {"LFBP_TILE_Y": "4", "LFBP_BAND": "2", "LFBP_PRODUCERS": "2"},
 ])
 @pytest.mark.parametrize("shape,dtype", [((55, 55, 11, 11, 2), np.float32), ((27, 20, 13, 5, 2), np.float64),
                                          ((66, 41, 21, 9, 1), np.float32), ((81, 12, 41, 3, 2), np.float32)])
@@ -171,6 +174,8 @@ def test_plan_variants_are_bit_exact(monkeypatch, env, shape, dtype):
         assert p["n_chunks"] > 1
     if "LFBP_PRODUCERS" in env:
         assert p["producers"] == int(env["LFBP_PRODUCERS"])
+    if "LFBP_TILE_Y" in env:
+        assert p["tile_y"] == min(int(env["LFBP_TILE_Y"]), shape[3])
     H = random_psf_like_reference(shape, density=0.9, seed=7, dtype=dtype)
     out = hprime_device(to_device(H))
     torch.cuda.synchronize()
