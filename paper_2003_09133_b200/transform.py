@@ -165,14 +165,21 @@ def compute_psf_from_backprojection(bp, device: int = 0):
 # --------------------------------------------------------------------------
 # device API
 
+def _f_strides(shape):
+    n_s, n_t, n_x, n_y, _ = shape
+    return (1, n_s, n_s * n_t, n_s * n_t * n_x, n_s * n_t * n_x * n_y)
+
+
 def _dims_of_tensor(t):
     """(n_s, n_t, n_x, n_y, n_z) of a CUDA tensor holding an F-ordered 5-D array."""
     if t.dim() != 5:
         raise InvalidDims(f"expected a 5-D tensor, got {t.dim()}-D")
-    if t.permute(4, 3, 2, 1, 0).is_contiguous():
-        return tuple(int(v) for v in t.shape)            # (n_s, ..., n_z), F strides
+    shape = tuple(t.shape)
+    st = t.stride()
+    if st == _f_strides(shape) or t.permute(4, 3, 2, 1, 0).is_contiguous():
+        return shape                                     # (n_s, ..., n_z), F strides
     if t.is_contiguous():
-        return tuple(int(v) for v in reversed(t.shape))  # (n_z, ..., n_s) C view
+        return tuple(reversed(shape))                    # (n_z, ..., n_s) C view
     raise ValueError("tensor must be Fortran-ordered (n_s..n_z) or C-contiguous (n_z..n_s)")
 
 
@@ -183,6 +190,20 @@ def _code_of(t) -> int:
     if size == 8:
         return _native.F64
     raise ValueError(f"element size {size} not supported (4 or 8 bytes)")
+
+
+_DIMS_CACHE: dict = {}
+
+
+def _dims_arg(shape):
+    """ctypes int64[5] of `shape`, cached (the device API is called per
+    launch; building the array is a measurable part of a small call)."""
+    d = _DIMS_CACHE.get(shape)
+    if d is None:
+        if len(_DIMS_CACHE) > 256:
+            _DIMS_CACHE.clear()
+        d = _DIMS_CACHE[shape] = _native.dims_array(shape)
+    return d
 
 
 def hprime_device(src, out=None, inverse: bool = False, z_range=None, stream=None):
@@ -197,16 +218,21 @@ def hprime_device(src, out=None, inverse: bool = False, z_range=None, stream=Non
         out = torch.empty_like(src)
     if out.shape != src.shape or out.stride() != src.stride() or out.dtype != src.dtype:
         raise ValueError("out must match src in shape, strides and dtype")
-    if out.device != src.device:
+    dev = src.device
+    if out.device != dev:
         raise ValueError("src and out must be on the same device")
     z0, z1 = (0, shape[4]) if z_range is None else (int(z_range[0]), int(z_range[1]))
     if stream is None:
-        stream = torch.cuda.current_stream(src.device)
-    handle = ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
-    with torch.cuda.device(src.device):
-        rc = _native.lib().lfbp_hprime_device(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(out.data_ptr()),
-                                              _native.dims_array(shape), _code_of(src), int(inverse),
-                                              z0, z1, handle)
+        stream = torch.cuda.current_stream(dev)
+    handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    lib = _native.lib()
+    args = (ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(out.data_ptr()), _dims_arg(shape), _code_of(src),
+            int(inverse), z0, z1, ctypes.c_void_p(handle))
+    if dev.index == torch.cuda.current_device():
+        rc = lib.lfbp_hprime_device(*args)
+    else:
+        with torch.cuda.device(dev):
+            rc = lib.lfbp_hprime_device(*args)
     _native.check(rc)
     return out
 
