@@ -212,6 +212,35 @@ def test_full_size_involution_on_device(cfg):
     assert involution_check(src) == (0, -1)
 
 
+def test_wide_shape_default_plan_matches_oracle():
+    """A shape with n_x > 32 runs its default plan with two producer warps
+    and the unit order in y blocks of 4 (37 y: ragged last block)."""
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device, plan
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    shape = (95, 95, 47, 37, 2)
+    p = plan(shape)
+    assert p["producers"] == 2 and p["tile_y"] == 4
+    H = random_psf_like_reference(shape, density=0.8, seed=95, dtype=np.float32)
+    out = hprime_device(to_device(H))
+    torch.cuda.synchronize()
+    assert to_host(out).tobytes() == fbytes(hprime_oracle(H))
+
+
+def test_reference_full_scale_acceptance_shape_involution():
+    """The reference's opt-in full-scale acceptance shape (181,181,95,55,1)
+    (test_acceptance.py:225-242): forward then inverse returns H byte for
+    byte, compared on the device (3 producer warps, y blocks of 4)."""
+    torch = _torch()
+    from paper_2003_09133_b200 import f_order_empty, plan
+    from paper_2003_09133_b200.verify import involution_check
+    shape = (181, 181, 95, 55, 1)
+    assert plan(shape)["producers"] == 3 and plan(shape)["tile_y"] == 4
+    src = f_order_empty(shape, torch.float32)
+    src.permute(4, 3, 2, 1, 0).reshape(-1).view(torch.int32).random_()
+    assert involution_check(src) == (0, -1)
+
+
 def test_empty_z_range_is_a_no_op():
     torch = _torch()
     from paper_2003_09133_b200 import hprime_device
