@@ -12,7 +12,8 @@ import threading
 
 from .errors import DimsError, EvenPixelDims, FormatError, InvalidDims, IoError, LfbpError, NativeError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhprime.so")
+# LFBP_LIB_PATH: load another build of the library (same-box A/B of kernel versions)
+LIB_PATH = os.environ.get("LFBP_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhprime.so")
 
 (OK, ERR_INVALID_DIMS, ERR_EVEN_PIXEL_DIMS, ERR_CUDA, ERR_ARGUMENT, ERR_UNSUPPORTED, ERR_FORMAT, ERR_IO,
  ERR_DIMS) = range(9)

@@ -105,7 +105,12 @@ __device__ __forceinline__ Unit decode_unit(const HpPlan& p, uint32_t u) {
     band = static_cast<int32_t>(u - r * p.nb_div.d);
     r2 = hp_div(p.ny_div, r);
     w.y = r - r2 * p.ny_div.d;
-  } else {  // consecutive units: neighbouring y (their output rows interleave in L2)
+  } else if (p.n_yblocks == 1) {  // consecutive units: neighbouring y (their output rows interleave in L2)
+    const uint32_t r = hp_div(p.ny_div, u);
+    w.y = u - r * p.ny_div.d;
+    r2 = hp_div(p.nb_div, r);
+    band = static_cast<int32_t>(r - r2 * p.nb_div.d);
+  } else {  // the same inside y blocks of tile_y (wide shapes)
     r2 = hp_div(p.zc_div, u);
     const uint32_t r = u - r2 * p.zc_div.d;
     const uint32_t yb = hp_div(p.yblk_div, r);
