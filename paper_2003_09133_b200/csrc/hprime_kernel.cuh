@@ -301,20 +301,32 @@ __device__ __forceinline__ void row_groups(typename Word<E>::T* o, int32_t g, in
     g += W;
   }
   const int32_t g_hi = last_full ? ng : ng - 1;
-  if (g < g_hi) {  // full groups, software-pipelined: load group k+1 before storing group k
-    T v[VE];
-    load_group<E, WRAP1>(v, a0, x0, n_x, step, nr);
-    for (g += W; g < g_hi; g += W) {
-      T* o_cur = o;
+  if (g < g_hi) {  // full groups, software-pipelined: load group k+1 before storing group k;
+                   // unrolled by two with alternating register sets (no copies between them)
+    T va[VE], vb[VE];
+    load_group<E, WRAP1>(va, a0, x0, n_x, step, nr);
+    for (;;) {
+      g += W;
+      if (g >= g_hi) {
+        st_vec<E>(o, va);
+        advance();
+        break;
+      }
+      T* oa = o;
       advance();
-      T vn[VE];
-      load_group<E, WRAP1>(vn, a0, x0, n_x, step, nr);
-      st_vec<E>(o_cur, v);
-#pragma unroll
-      for (int q = 0; q < VE; ++q) v[q] = vn[q];
+      load_group<E, WRAP1>(vb, a0, x0, n_x, step, nr);
+      st_vec<E>(oa, va);
+      g += W;
+      if (g >= g_hi) {
+        st_vec<E>(o, vb);
+        advance();
+        break;
+      }
+      T* ob = o;
+      advance();
+      load_group<E, WRAP1>(va, a0, x0, n_x, step, nr);
+      st_vec<E>(ob, vb);
     }
-    st_vec<E>(o, v);
-    advance();
   }
   if (g < ng) masked();  // trailing partial group
 }
