@@ -140,6 +140,7 @@ Knobs default_knobs(int64_t moved_bytes) {
 const Knobs kCandidates[] = {
     {3, 48, 8, 8},  {4, 48, 12, 16}, {4, 48, 8, 8},  {4, 48, 8, 16}, {2, 96, 8, 16},
     {3, 64, 8, 32}, {4, 48, 16, 16}, {2, 96, 8, 8},  {4, 16, 8, 0},  {4, 16, 4, 4},
+    {2, 96, 12, 32},  // C4 with the v7 loop: J = 3, +3 % over the former best (profiles/r01_sweep_v7.jsonl)
 };
 // Small problems (8-256 MB moved) are latency-bound: smaller stages (narrower
 // t-bands, several CTAs per SM) and short-row sub-warps; measured on the
