@@ -20,6 +20,7 @@
 // (test_projector.py:67-82).  All arrays are F-ordered; volumes / images are
 // float64.
 #pragma once
+#include <cuda.h>  // CUtensorMap
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -370,6 +371,154 @@ __global__ void __launch_bounds__(128, poly_tile_min_blocks(RL)) poly_tile_kerne
         }
       }
     }
+  }
+  const int32_t k = k0 + tk;
+  const int32_t l = L0 + tl * RL;
+  const int32_t X = px + q.n_x * k;
+#pragma unroll
+  for (int j = 0; j < RL; ++j) {
+    const int32_t Y = py + q.n_y * (l + j);
+    if (k < pg.kc && l + j < pg.lc && X < q.nvx && Y < q.nvy)
+      out[X + int64_t(Y) * q.nvx + int64_t(zout) * q.nvx * q.nvy] = acc[j];
+  }
+}
+
+// ---- TMA double-buffered variant of poly_tile_kernel -----------------------
+// Same sums and the same per-class compute loop.  The class's sub-image
+// window is loaded by ONE thread as a 3-D tiled TMA box (kk, ll, sub-image)
+// into one of two shared buffers while the block computes the previous class
+// from the other, so the window fill no longer stalls the FP64 loop.  Cells
+// outside the padded sub-image are zero-filled by the TMA unit.  The box's
+// first column must be 16-byte aligned (an odd double offset faults with
+// "illegal instruction"), so the window starts one column early when its
+// origin is odd and the compute reads from column `shift`.  Shared layout:
+// 2 mbarriers (128 B), two tile buffers of th x p doubles at 128-byte aligned
+// offsets (p = box width, even), then the mmax x nmax taps.
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+struct PolyCls {
+  int32_t r2, a0, ryy, rxx, row_base, col_base, M, N;
+};
+
+__device__ __forceinline__ PolyCls poly_class(int32_t c, const ProjGeom& q, const PolyGeom& pg, const PolyTile& tg,
+                                              int32_t px, int32_t py, int32_t na0, int32_t L0, int32_t k0) {
+  PolyCls g;
+  g.r2 = c / na0;
+  g.a0 = c - g.r2 * na0;
+  g.N = (q.n_t - g.r2 + q.n_y - 1) / q.n_y;
+  g.M = (q.n_s - g.a0 + q.n_x - 1) / q.n_x;
+  const int32_t rho_y = tg.conv ? py + q.c_t - g.r2 : py - q.c_t + g.r2;
+  g.ryy = ((rho_y % q.n_y) + q.n_y) % q.n_y;
+  g.row_base = floordiv(rho_y, q.n_y) + pg.hy + L0 - (tg.conv ? g.N - 1 : 0);
+  const int32_t rho_x = tg.conv ? px + q.c_s - g.a0 : px - q.c_s + g.a0;
+  g.rxx = ((rho_x % q.n_x) + q.n_x) % q.n_x;
+  g.col_base = floordiv(rho_x, q.n_x) + pg.hx + k0 - (tg.conv ? g.M - 1 : 0);
+  return g;
+}
+
+template <typename T, int RL>
+__global__ void __launch_bounds__(128, poly_tile_min_blocks(RL))
+    poly_tma_kernel(const __grid_constant__ CUtensorMap tmap, const T* __restrict__ K, double* __restrict__ out,
+                    const ProjGeom q, const PolyGeom pg, const PolyTile tg, int32_t forward) {
+  extern __shared__ __align__(128) uint8_t psm_raw[];
+  const int32_t tile_elems = tg.th * tg.p;
+  const int32_t tile_stride = ((tile_elems * 8 + 127) / 128) * 128;   // bytes, 128-aligned buffers
+  uint64_t* bars = reinterpret_cast<uint64_t*>(psm_raw);
+  double* tiles = reinterpret_cast<double*>(psm_raw + 128);
+  double* ks = reinterpret_cast<double*>(psm_raw + 128 + 2 * tile_stride);
+  const int32_t nthr = tg.tk * tg.tlt;
+  const int32_t tid = threadIdx.x;
+  const int32_t tl = tid / tg.tk, tk = tid - tl * tg.tk;
+  const int32_t n_ph = q.n_x * q.n_y;
+  const int32_t ph = blockIdx.z % n_ph;
+  const int32_t zout = blockIdx.z / n_ph;
+  const int32_t px = ph % q.n_x, py = ph / q.n_x;
+  const int32_t k0 = blockIdx.x * tg.tk;
+  const int32_t L0 = blockIdx.y * tg.tlt * RL;
+  const int64_t pat = int64_t(q.n_s) * q.n_t;
+  const T* Kz = K + (int64_t(zout) * n_ph + ph) * pat;
+  const int32_t sub0 = forward ? zout * n_ph : 0;   // first sub-image of this block's input plane
+  const int32_t na0 = min(q.n_x, q.n_s);
+  const int32_t ncls = min(q.n_y, q.n_t) * na0;
+  const uint32_t tile_bytes = uint32_t(tile_elems) * 8u;
+  const uint32_t tiles_s = smem_u32(tiles);
+  if (tid == 0) {
+    mbar_init(smem_u32(&bars[0]), 1);
+    mbar_init(smem_u32(&bars[1]), 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0 && ncls > 0) {
+    const PolyCls g = poly_class(0, q, pg, tg, px, py, na0, L0, k0);
+    mbar_arrive_expect_tx(smem_u32(&bars[0]), tile_bytes);
+    tma_load_3d(tiles_s, &tmap, g.col_base & ~1, g.row_base, sub0 + g.ryy * q.n_x + g.rxx, smem_u32(&bars[0]));
+  }
+  double acc[RL];
+#pragma unroll
+  for (int j = 0; j < RL; ++j) acc[j] = 0.0;
+  for (int32_t c = 0; c < ncls; ++c) {
+    const int32_t buf = c & 1;
+    // the other buffer was last read by class c - 1, done before the
+    // trailing barrier of the previous iteration
+    if (tid == 0 && c + 1 < ncls) {
+      const PolyCls g = poly_class(c + 1, q, pg, tg, px, py, na0, L0, k0);
+      const uint32_t bar = smem_u32(&bars[buf ^ 1]);
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(bar, tile_bytes);
+      tma_load_3d(tiles_s + uint32_t(buf ^ 1) * uint32_t(tile_stride), &tmap, g.col_base & ~1, g.row_base,
+                  sub0 + g.ryy * q.n_x + g.rxx, bar);
+    }
+    const PolyCls g = poly_class(c, q, pg, tg, px, py, na0, L0, k0);
+    const int32_t r2 = g.r2, a0 = g.a0, M = g.M, N = g.N;
+    const int32_t shift = g.col_base & 1;
+    const T* Kc = tg.conv ? K + (int64_t(zout) * n_ph + g.rxx + int64_t(q.n_x) * g.ryy) * pat : Kz;
+    for (int32_t e = tid; e < tg.mmax * tg.nmax; e += nthr) {
+      const int32_t ap = e / tg.nmax, n = e - ap * tg.nmax;
+      double v = 0.0;
+      if (ap < M && n < N) {
+        const int32_t ta = tg.conv ? M - 1 - ap : ap, tb = tg.conv ? N - 1 - n : n;
+        v = static_cast<double>(Kc[(a0 + q.n_x * ta) + int64_t(q.n_s) * (r2 + q.n_y * tb)]);
+      }
+      ks[e] = v;
+    }
+    __syncthreads();  // taps visible
+    mbar_wait(smem_u32(&bars[buf]), uint32_t((c >> 1) & 1));
+    const double* tile = tiles + int64_t(buf) * (tile_stride / 8) + shift;
+    for (int32_t ap = 0; ap < M; ++ap) {
+      const double* col = tile + (tl * RL) * tg.p + tk + ap;
+      const double* kv = ks + ap * tg.nmax;
+      double w[RL];
+#pragma unroll
+      for (int j = 0; j < RL - 1; ++j) w[j] = col[j * tg.p];
+      const double* rowp = col + (RL - 1) * tg.p;
+      int32_t n = 0;
+      for (; n + RL <= N; n += RL) {
+#pragma unroll
+        for (int t = 0; t < RL; ++t) {
+          w[(RL - 1 + t) % RL] = *rowp;
+          rowp += tg.p;
+          const double v = kv[n + t];
+#pragma unroll
+          for (int j = 0; j < RL; ++j) acc[j] = fma(w[(j + t) % RL], v, acc[j]);
+        }
+      }
+      for (; n < N; ++n) {
+        w[RL - 1] = *rowp;
+        rowp += tg.p;
+        const double v = kv[n];
+#pragma unroll
+        for (int j = 0; j < RL; ++j) acc[j] = fma(w[j], v, acc[j]);
+#pragma unroll
+        for (int j = 0; j < RL - 1; ++j) w[j] = w[j + 1];
+      }
+    }
+    __syncthreads();  // tile[buf] and ks free for reuse
   }
   const int32_t k = k0 + tk;
   const int32_t l = L0 + tl * RL;
