@@ -1,31 +1,43 @@
 #!/usr/bin/env python
 """Benchmark of the H -> H' rearrangement (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--weak]
+                    [--impl ours|reference]
 
-One step = one pass of the K1 kernel over one whole workload (C2 by default,
-BASELINE.json configs[1]: H float32 (195,195,15,15,51), 1.75 GB in + out),
-inputs resident in HBM.  Under torchrun (N > 1) every rank owns one C2-shaped
-depth stack (z-slab) of its own -- weak scaling, no collective on the data
-path; the NCCL process group only carries the barriers and the max-over-ranks
-time.  ``--config C3 --strong`` instead shards one C3 array's planes over the
-ranks.
+Workload: C5 by default -- BASELINE.json configs[4], H float32
+(631,631,21,21,101), 70.9 GB in + 70.9 GB out resident on one GPU, the
+largest single-GPU configuration.  One step = one pass of the K1 kernel over
+this rank's planes, inputs resident in HBM (generated on the device by K6,
+bit-identical to the host generator).
 
-Printed by rank 0, one JSON line:
+Multi-GPU (torchrun, one process per GPU): the north_star z-split -- the
+config's n_z planes are split into contiguous slabs, one per rank
+(``shard_planes``), and every rank runs K1 on its slab; no collective on the
+data path (NCCL only carries barriers and the max-over-ranks time).  Total
+work is fixed, so ``scaling`` is "strong"; the N=1 line is the single-GPU
+headline.  ``--weak`` instead gives every rank a full replica.
+
+Rank 0 prints one JSON line:
   value        algorithmic GB/s (bytes read + written, 2*N*itemsize per step)
-               over all ranks / max-over-ranks device time (CUDA events)
+               summed over ranks / max-over-ranks device time (CUDA events)
   roofline     dominant kernel (K1) achieved GB/s vs MEASURED_PEAKS.json
-  e2e          same metric through the C-ABI host path (pinned host buffers,
-               H2D + kernel + D2H every step, wall clock around the
-               synchronous call)
-  cpu_baseline the reference algorithm (oracle/hprime_oracle.py, the numpy
-               restatement of lfbp.compute_backprojection) on a bounded
-               sample, all host threads over depth planes
-``--impl reference`` prints the same metric for that CPU arm alone.
+  e2e          same metric through the C-ABI host path lfbp_hprime_host on
+               each rank's whole slab: pinned host H -> chunked H2D / K1 /
+               D2H -> pinned host H' every step, wall clock around the
+               synchronous call, max over ranks
+  shards       per-rank planes, kernel ms and digest verification
+  cpu_baseline the UNMODIFIED reference lfbp.compute_backprojection
+               (baseline/_ref, single-threaded numpy as shipped) on one plane
+               of the same config (chunked: planes are independent);
+               cpu_baseline_port: the oracle's numpy restatement on all host
+               threads
+``--impl reference`` prints the same metric for the CPU arm alone (the
+oracle port, every host thread, a bounded plane sample of the same config).
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import hashlib
 import json
 import os
@@ -42,6 +54,7 @@ sys.path.insert(0, ROOT)
 METRIC = "H' build GB/s (bytes read+written)"
 L2_BYTES = 126 << 20
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 def _peaks():
@@ -104,11 +117,9 @@ class ClockSampler:
             self._th.join()
 
     def summary(self):
-        if not self.ok or not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                    "samples": len(self.samples), "source": "nvml"}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
+        med = statistics.median(self.samples) if self.ok and self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "nvml"}
 
 
 def _dtype_tag(dtype) -> str:
@@ -123,57 +134,114 @@ def _dist():
     return rank, world, local
 
 
-def cpu_sample(w, planes: int, threads: int, reps: int):
-    """Time the reference algorithm (numpy restatement) on `planes` planes of
-    workload `w` with `threads` host threads; returns (seconds, bytes r+w)."""
-    from oracle.hprime_oracle import hprime_oracle
+def _workload_tag(w) -> str:
+    return f"{w.name} {w.shape} {np.dtype(w.dtype).name} seed {w.seed}"
+
+
+def _golden_plane_digests(w):
+    path = os.path.join(ROOT, "tests", "golden", f"digests_{w.name}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)["hprime_plane_sha256"]
+
+
+# ---------------------------------------------------------------- CPU legs
+
+def _threads() -> int:
+    return max(1, os.cpu_count() or 1)
+
+
+def cpu_reference_one_plane(w, z: int):
+    """The unmodified reference (baseline/_ref lfbp, single-threaded numpy as
+    shipped) on plane z of the workload; returns the cpu_baseline object or
+    None when the reference is not installed."""
+    if not os.path.isdir(os.path.join(REF_DIR, "lfbp")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import lfbp  # noqa: E402  (the reference package, unmodified)
+
     from paper_2003_09133_b200.synth import baseline_psf
-    H = baseline_psf(w, 0, planes)
-    hprime_oracle(H[..., :1], threads=1)   # warm the index tables
+    H = baseline_psf(w, z, z + 1)
+    psf = lfbp.PsfArray._wrap(lfbp.Dims5(*H.shape), H)
+    t = time.perf_counter()
+    bp = lfbp.compute_backprojection(psf)
+    secs = time.perf_counter() - t
+    want = _golden_plane_digests(w)
+    ok = None if want is None else hashlib.sha256(bp.data.tobytes(order="F")).hexdigest() == want[z]
+    return {"value": round(2 * H.nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": f"plane {z} of {w.shape[4]} of {w.name} (chunked: planes are independent, "
+                      f"reference test_transform.py:141-154), one run",
+            "seconds": round(secs, 3),
+            "what": "lfbp.compute_backprojection from baseline/_ref (the unmodified reference, "
+                    "single-threaded numpy as shipped: reference bench.py:99-105)",
+            "host_threads_available": _threads(), "matches_reference_digest": ok}
+
+
+def cpu_port_sample(w, planes: int, threads: int, reps: int = 1):
+    """The oracle's numpy restatement on `planes` planes with `threads` host
+    threads (split over planes and output columns); (seconds, bytes r+w)."""
+    from oracle.hprime_oracle import hprime_oracle_split
+    from paper_2003_09133_b200.synth import baseline_psf
+    z0 = max(0, w.shape[4] // 2 - planes // 2)
+    H = baseline_psf(w, z0, z0 + planes)
+    hprime_oracle_split(H[..., :1], threads)   # warm the index tables
     times = []
     for _ in range(reps):
         t = time.perf_counter()
-        hprime_oracle(H, threads=threads)
+        hprime_oracle_split(H, threads)
         times.append(time.perf_counter() - t)
-    return statistics.median(times), 2 * H.nbytes
+    return statistics.median(times), 2 * H.nbytes, z0
+
+
+def _port_planes(w, requested: int) -> int:
+    """Planes per CPU sample: ~1.5 GB of H (C5: 2 planes, C2: 16)."""
+    if requested > 0:
+        return min(w.shape[4], requested)
+    return max(1, min(w.shape[4], (3 << 29) // (w.plane_elems * w.itemsize)))
 
 
 def run_reference(args, w):
+    """--impl reference: the CPU arm (the oracle port, every host thread) on a
+    bounded plane sample of the same workload, per step."""
     rank, world, _ = _dist()
     if world > 1 and rank != 0:
         return 0
-    planes = min(w.shape[4], max(args.cpu_planes, os.cpu_count() or 1))
-    threads = min(os.cpu_count() or 1, planes)
-    from oracle.hprime_oracle import hprime_oracle
+    from oracle.hprime_oracle import hprime_oracle_split
     from paper_2003_09133_b200.synth import baseline_psf
-    H = baseline_psf(w, 0, planes)
+    planes = _port_planes(w, args.cpu_planes)
+    threads = _threads()
+    z0 = max(0, w.shape[4] // 2 - planes // 2)
+    H = baseline_psf(w, z0, z0 + planes)
     for _ in range(args.warmup):
-        hprime_oracle(H, threads=threads)
+        hprime_oracle_split(H, threads)
     times = []
     for _ in range(args.steps):
         t = time.perf_counter()
-        hprime_oracle(H, threads=threads)
+        hprime_oracle_split(H, threads)
         times.append(time.perf_counter() - t)
     total = sum(times)
     gbs = 2 * H.nbytes * args.steps / total / 1e9
-    sample = f"{planes} of {w.shape[4]} planes of {w.name} {w.shape} per step (planes are independent)"
+    sample = (f"planes [{z0}, {z0 + planes}) of {w.shape[4]} of {w.name} per step (chunked: planes are "
+              f"independent, reference test_transform.py:141-154)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": _dtype_tag(w.dtype), "data": "synthetic (seeded BASELINE law)",
-        "config": {"workload": f"{w.name} {w.shape} {np.dtype(w.dtype).name} seed {w.seed}",
-                   "sample_planes": planes},
+        "higher_is_better": True, "scaling": "strong" if not args.weak else "weak", "vs_baseline": None,
+        "dtype": _dtype_tag(w.dtype), "data": "synthetic (seeded BASELINE.json law, see synth.py)",
+        "config": {"workload": _workload_tag(w), "sample_planes": planes},
         "helems_per_s": round(H.size * args.steps / total, 1),
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": sample,
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample,
                          "what": "oracle/hprime_oracle.py: numpy restatement of lfbp.compute_backprojection "
-                                 "(transform.py:113-135), depth planes split over host threads"},
+                                 "(transform.py:113-135), planes and output columns split over host threads"},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
+
+# ---------------------------------------------------------------- GPU arm
 
 def _max_over_ranks(x: float, world: int, device) -> float:
     import torch
@@ -184,26 +252,70 @@ def _max_over_ranks(x: float, world: int, device) -> float:
     return float(t.item())
 
 
-def _verify_against_golden(out, w, shape):
-    from paper_2003_09133_b200.verify import plane_digests
-    path = os.path.join(ROOT, "tests", "golden", f"digests_{w.name}.json")
-    if not os.path.exists(path) or tuple(shape) != tuple(w.shape):
+def _gather_objects(obj, world: int):
+    if world == 1:
+        return [obj]
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
+class HostBuffer:
+    """One host array of `nbytes` for the e2e leg: page-locked from the
+    library allocator (lfbp_host_alloc: huge pages, registered) when the host
+    can pin it, else pageable (then the host path stages it)."""
+
+    def __init__(self, nbytes: int, pinned: bool):
+        from paper_2003_09133_b200.errors import NativeError
+        from paper_2003_09133_b200.transform import _PinnedBlock
+        self.pinned = False
+        if pinned:
+            try:
+                self.arr = np.asarray(_PinnedBlock(nbytes))[:nbytes]
+                self.pinned = True
+            except NativeError:
+                pass
+        if not self.pinned:
+            self.arr = np.empty(nbytes, dtype=np.uint8)
+            self.arr[::4096] = 0   # fault the pages in outside the timed region
+
+    def free(self):
+        from paper_2003_09133_b200 import _native
+        self.arr = None            # the block goes back to the library (released below)
+        _native.lib().lfbp_host_cache_release()
+
+
+def _host_plane_digests(buf: np.ndarray, plane_bytes: int, n_planes: int) -> list[str]:
+    import concurrent.futures as cf
+
+    def one(z):
+        return hashlib.sha256(memoryview(buf[z * plane_bytes:(z + 1) * plane_bytes])).hexdigest()
+
+    with cf.ThreadPoolExecutor(min(16, _threads())) as pool:
+        return list(pool.map(one, range(n_planes)))
+
+
+def _all_verified(shard_info):
+    """True when every rank with planes matched the reference digests, False
+    if one did not, None when verification was skipped."""
+    vals = [s["verified"] for s in shard_info if s["planes"][1] > s["planes"][0]]
+    if not vals or any(v is None for v in vals):
         return None
-    with open(path) as f:
-        want = json.load(f)["hprime_plane_sha256"]
-    return plane_digests(out, shape) == want
+    return all(vals)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--strong", action="store_true", help="shard one array's planes over ranks")
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--weak", action="store_true", help="every rank a full replica instead of the z-split")
+    ap.add_argument("--strong", action="store_true", help="(default) z-split of one array over the ranks")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-planes", type=int, default=8)
+    ap.add_argument("--cpu-planes", type=int, default=0, help="planes per CPU sample (0: about 1.5 GB)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -225,8 +337,9 @@ def main():
     import torch.distributed as dist
 
     from paper_2003_09133_b200 import _native, f_order_empty, hprime_device, plan
-    from paper_2003_09133_b200.shard import shard_planes
-    from paper_2003_09133_b200.synth import baseline_psf
+    from paper_2003_09133_b200.shard import imbalance, shard_planes
+    from paper_2003_09133_b200.synth import baseline_psf_device
+    from paper_2003_09133_b200.verify import plane_digests
 
     rank, world, local = _dist()
     # one process per GPU; LFBP_BENCH_BACKEND=gloo (+ device = local % count)
@@ -240,23 +353,27 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+    red_dev = dev if backend == "nccl" else "cpu"
 
     # this rank's slab
-    if args.strong:
-        z0, z1 = shard_planes(w.shape[4], world, rank)
-    else:
+    if args.weak:
         z0, z1 = 0, w.shape[4]
-    shape = (*w.shape[:4], z1 - z0)
+    else:
+        z0, z1 = shard_planes(w.shape[4], world, rank)
+    nz = z1 - z0
+    shape = (*w.shape[:4], nz)
     tdt = torch.float32 if w.itemsize == 4 else torch.float64
-    host_in = torch.empty(w.plane_elems * (z1 - z0), dtype=tdt, pin_memory=True)
-    hin = host_in.numpy().reshape(shape, order="F")
-    baseline_psf(w, z0, z1, out=hin)
-    src = f_order_empty(shape, tdt, dev)
-    src.permute(4, 3, 2, 1, 0).reshape(-1).copy_(host_in)
-    out = f_order_empty(shape, tdt, dev)
-    n_elems = w.plane_elems * (z1 - z0)
+    n_elems = w.plane_elems * nz
+    plane_bytes = w.plane_elems * w.itemsize
     step_bytes = 2 * n_elems * w.itemsize
+    src = f_order_empty(shape, tdt, dev)
+    out = f_order_empty(shape, tdt, dev)
     stream = torch.cuda.current_stream(dev)
+    t_setup = time.perf_counter()
+    if nz:
+        baseline_psf_device(w, z0, z1, out=src)
+    torch.cuda.synchronize(dev)
+    setup_s = time.perf_counter() - t_setup
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -264,14 +381,19 @@ def main():
             dist.barrier(device_ids=[local]) if backend == "nccl" else dist.barrier()
         torch.cuda.synchronize(dev)
 
+    def step():
+        if nz:
+            hprime_device(src, out=out, stream=stream)
+
+    # the first call autotunes the plan on these buffers (lfbp_hprime_device)
     for _ in range(args.warmup):
-        hprime_device(src, out=out, stream=stream)
+        step()
     barrier()
 
     # inputs smaller than 2x L2 (C1): flush L2 between steps by writing a
     # 512 MB buffer outside the per-step events, and time the steps only
     flush = None
-    if step_bytes < 2 * L2_BYTES:
+    if step_bytes < 2 * L2_BYTES and nz:
         flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -285,30 +407,37 @@ def main():
             if flush is not None:
                 flush.fill_(k & 0xff)
             starts[k].record(stream)
-            hprime_device(src, out=out, stream=stream)
+            step()
             ends[k].record(stream)
         t1.record(stream)
         barrier()
     launches = _native.launch_count() - l0
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     elapsed_ms = sum(kern_ms) if flush is not None else t0.elapsed_time(t1)
-    max_ms = _max_over_ranks(elapsed_ms, world, dev if backend == "nccl" else "cpu")
+    max_ms = _max_over_ranks(elapsed_ms, world, red_dev)
 
+    # every rank checks its planes against the reference's per-plane digests
     verified = None
-    if not args.no_verify and rank == 0:
-        verified = _verify_against_golden(out, w, shape)
+    if not args.no_verify and nz:
+        want = _golden_plane_digests(w)
+        if want is not None:
+            verified = plane_digests(out, shape, threads=min(16, _threads())) == want[z0:z1]
+        torch._C._host_emptyCache()   # the digest staging buffers, before the e2e leg pins its own
 
-    # end-to-end through the C-ABI host path, pinned host buffers
+    # end to end through the C-ABI host path on this rank's whole slab
     e2e = None
-    if not args.no_e2e:
-        import ctypes
-        host_out = torch.empty_like(host_in, pin_memory=True)
+    if not args.no_e2e and nz:
+        nbytes = n_elems * w.itemsize
+        hin = HostBuffer(nbytes, pinned=True)
+        hout = HostBuffer(nbytes, pinned=hin.pinned)
+        torch.from_numpy(hin.arr).copy_(src.permute(4, 3, 2, 1, 0).reshape(-1).view(torch.uint8))
         code = _native.F32 if w.itemsize == 4 else _native.F64
         dvec = _native.dims_array(shape)
+        lib = _native.lib()
 
         def host_call():
-            rc = _native.lib().lfbp_hprime_host(ctypes.c_void_p(host_in.data_ptr()),
-                                                ctypes.c_void_p(host_out.data_ptr()), dvec, code, 0, local, 0)
+            rc = lib.lfbp_hprime_host(ctypes.c_void_p(hin.arr.ctypes.data), ctypes.c_void_p(hout.arr.ctypes.data),
+                                      dvec, code, 0, local, _native.HOST_STAGE)
             _native.check(rc)
 
         host_call()
@@ -317,24 +446,41 @@ def main():
         for _ in range(args.e2e_steps):
             host_call()
         barrier()
-        e2e_s = time.perf_counter() - t
-        e2e_s = _max_over_ranks(e2e_s, world, dev if backend == "nccl" else "cpu")
-        ok = hashlib.sha256(host_out.numpy().tobytes()).hexdigest() == hashlib.sha256(
-            out.permute(4, 3, 2, 1, 0).contiguous().view(-1).cpu().numpy().tobytes()).hexdigest()
-        e2e = {"value": round(world * step_bytes * args.e2e_steps / e2e_s / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": n_elems * w.itemsize, "d2h_bytes_per_step": n_elems * w.itemsize,
+        e2e_s = _max_over_ranks(time.perf_counter() - t, world, red_dev)
+        want = _golden_plane_digests(w)
+        ok = (None if want is None else
+              _host_plane_digests(hout.arr, plane_bytes, nz) == want[z0:z1])
+        e2e_total = step_bytes if args.weak else 2 * w.nbytes
+        e2e = {"value": round((world if args.weak else 1) * e2e_total * args.e2e_steps / e2e_s / 1e9, 3),
+               "unit": "GB/s", "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "bytes_per_step_note": "per rank (this rank's slab)",
                "steps": args.e2e_steps, "ms_per_step": round(1e3 * e2e_s / args.e2e_steps, 3),
-               "path": "lfbp_hprime_host (C-ABI): pinned host H -> chunked H2D/K1/D2H on 3 streams -> pinned host H'",
-               "matches_device_result": ok, "timing": "wall clock around the synchronous call, max over ranks"}
+               "path": "lfbp_hprime_host (C-ABI) on the rank's whole slab: host H -> chunked H2D/K1/D2H on "
+                       "3 streams -> host H'",
+               "host_buffers": "pinned (lfbp_host_alloc)" if hin.pinned else
+                               "pageable, staged through pinned chunks (LFBP_HOST_STAGE)",
+               "matches_reference_digests": ok, "timing": "wall clock around the synchronous call, max over ranks"}
+        hin.free()
+        hout.free()
 
-    cpu = None
+    shard_info = _gather_objects({"rank": rank, "planes": [z0, z1], "kernel_ms_avg": round(statistics.mean(kern_ms), 4)
+                                  if kern_ms and nz else 0.0, "verified": verified}, world)
+
+    cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        planes = min(w.shape[4], max(args.cpu_planes, os.cpu_count() or 1))
-        threads = min(os.cpu_count() or 1, planes)
-        secs, nbytes = cpu_sample(w, planes, threads, reps=3)
-        cpu = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": f"{planes} of {w.shape[4]} planes of {w.name}, median of 3, depth planes over {threads} threads",
-               "what": "oracle/hprime_oracle.py (numpy restatement of lfbp.compute_backprojection)"}
+        try:
+            cpu = cpu_reference_one_plane(w, w.shape[4] // 2)
+        except Exception as e:   # the reference leg must not sink the bench line
+            cpu = {"error": f"{type(e).__name__}: {e}"}
+        planes = _port_planes(w, args.cpu_planes)
+        threads = _threads()
+        secs, nbytes, zs = cpu_port_sample(w, planes, threads)
+        cpu_port = {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                    "sample": f"planes [{zs}, {zs + planes}) of {w.name}, planes and output columns over {threads} "
+                              f"threads (chunked)",
+                    "what": "oracle/hprime_oracle.py (numpy restatement of lfbp.compute_backprojection)"}
+        if cpu is None or "error" in cpu:
+            cpu, cpu_port = cpu_port, cpu
 
     if rank == 0:
         peak, peak_src = _peaks()
@@ -350,31 +496,38 @@ def main():
                     traffic = pj.get("dram_bytes_per_launch")
             except (OSError, ValueError):
                 pass
-        value = world * step_bytes * args.steps / (max_ms * 1e-3) / 1e9
+        total_bytes = (world if args.weak else 1) * (step_bytes if args.weak else 2 * w.nbytes)
+        value = total_bytes * args.steps / (max_ms * 1e-3) / 1e9
         p = plan(shape, w.dtype)
+        sizes = [s["planes"][1] - s["planes"][0] for s in shard_info]
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
-            "dtype": _dtype_tag(w.dtype), "data": "synthetic (seeded BASELINE.json law, see synth.py)",
-            "config": {"workload": f"{w.name} {w.shape} {np.dtype(w.dtype).name} seed {w.seed}",
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
+            "dtype": _dtype_tag(w.dtype), "data": "synthetic (seeded BASELINE.json law, generated on the device "
+                                                  "by K6, bit-identical to synth.py)",
+            "config": {"workload": _workload_tag(w),
                        "per_rank_shape": list(shape),
-                       "parallelism": f"z-slab x{world}, no collective on the data path",
+                       "parallelism": (f"z-slab x{world} (contiguous plane ranges), no collective on the data path"
+                                       if not args.weak else f"replica x{world}, no collective on the data path"),
                        "l2": (f"inputs larger than L2 ({n_elems * w.itemsize / 1e9:.2f} GB per array vs 0.126 GB)"
                               if flush is None else
                               "L2 flushed between steps (512 MB write outside the per-step events); "
                               "value = bytes / sum of per-step kernel times"),
                        "kernel_plan": p},
-            "helems_per_s": round(world * n_elems * args.steps / (max_ms * 1e-3), 1),
+            "helems_per_s": round(total_bytes / (2 * w.itemsize) * args.steps / (max_ms * 1e-3), 1),
             "frac_of_8tbs_nominal": round(value / world / 8000.0, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "kernel": "hp::hprime_kernel (K1)", "kernel_ms_avg": round(avg_kern_ms, 4),
                          "kernel_ms_min": round(min(kern_ms), 4),
                          "algorithmic_bytes_per_launch": step_bytes},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "first_timed_launch": l0,
-            "clocks": clk.summary(),
-            "verified_vs_reference_digests": verified,
+            "shards": {"planes_per_rank": sizes, "imbalance_max_over_mean": round(imbalance(w.shape[4], world), 4)
+                       if not args.weak else 1.0, "per_rank": shard_info},
+            "cpu_baseline": cpu, "cpu_baseline_port": cpu_port, "e2e": e2e, "gpu_launches": launches,
+            "first_timed_launch": l0, "clocks": clk.summary(),
+            "verified_vs_reference_digests": _all_verified(shard_info),
+            "setup_s": round(setup_s, 2),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -74,7 +74,13 @@ int64_t lfbp_dropped_source_count(const int64_t dims[5]);
  * n_s and n_t only; otherwise LFBP_ERR_EVEN_PIXEL_DIMS) for depth planes
  * [z_begin, z_end) of device arrays `src` and `dst` that both hold the WHOLE
  * (n_s, n_t, n_x, n_y, n_z) array, 16-byte aligned, non-overlapping.
- * Asynchronous on `stream`; the caller synchronises. */
+ * Asynchronous on `stream`; the caller synchronises -- except the FIRST call
+ * for a plane shape / element size / device / size class (launches moving
+ * >= 8 MB) with no tuned plan: that call runs the autotuner on `src`/`dst`
+ * first (40-60 timed launches with host synchronisations on `stream`; about
+ * 1.4 s on C5) and so returns only after they finish.  Call lfbp_tune()
+ * beforehand to keep every call asynchronous; LFBP_AUTOTUNE=0 disables the
+ * tuner (untuned default plan). */
 int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse,
                        int64_t z_begin, int64_t z_end, void* stream);
 
@@ -86,6 +92,25 @@ int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dt
  * Synchronous: returns when dst is complete. */
 int lfbp_hprime_host(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse,
                      int device, int flags);
+
+/* Tune the kernel plan for `dims` / `dtype` on `device` ahead of time, on
+ * library-owned scratch buffers (at most ~4 GB each): for launches of
+ * `z_count` planes (<= 0: all n_z) and for one chunk of the host pipeline.
+ * Synchronous.  Afterwards lfbp_hprime_device never synchronises, and
+ * lfbp_hprime_host / _multi / the LF5 path use the tuned chunk plan (they
+ * never tune by themselves).  Plans are cached per process. */
+int lfbp_tune(const int64_t dims[5], int dtype, int device, int64_t z_count);
+
+/* The autotuner's candidate plans for size class 1 (launches moving
+ * >= 256 MB) or 0 (8-256 MB): writes up to `max_n` records of 4 int32
+ * (smem stages, stage KB, consumer warps, lanes per row; 0 = by row length)
+ * into `knobs` (may be NULL) and returns the number of candidates.  No GPU. */
+int lfbp_plan_candidates(int size_class, int32_t* knobs, int max_n);
+
+/* memcpy of `bytes` split over `threads` host threads (<= 0: the library's
+ * staging pool, 3/4 of the host threads): the copy engine of the pageable
+ * staging path.  No GPU. */
+int lfbp_host_copy(void* dst, const void* src, int64_t bytes, int threads);
 
 /* Host-to-host H' with the z-planes split into contiguous slabs, one per
  * listed device, all devices running concurrently; no inter-GPU traffic.
@@ -177,6 +202,18 @@ int lfbp_safe_divide_peak_device(const double* num, const double* den, double* o
 int lfbp_rl_update_device(double* g, const double* back, const double* norm, int64_t n, double eps,
                           const double* peak, void* stream);
 
+/* Seeded synthetic H planes on the device (bench / test input generation,
+ * not the hot path; K6): `n_planes` planes of shape (n_s, n_t, n_x, n_y)
+ * into `dst` (F order, planes contiguous), bit-identical to the numpy
+ * generator paper_2003_09133_b200.synth.baseline_plane.  Per plane p:
+ * pcg_state[4p..4p+3] = the numpy PCG64 state (lo, hi) and increment
+ * (lo, hi) before the plane's first draw; tab_s[p*n_s*n_x + s + n_s*x] and
+ * tab_t[p*n_t*n_y + t + n_t*y] the per-axis factors; value
+ * (u * tab_s) * tab_t, or with disc_r2 != NULL: u if tab_s + tab_t <=
+ * disc_r2[p], else 0.  All pointers are device pointers.  Asynchronous. */
+int lfbp_synth_planes_device(void* dst, int dtype, const int64_t dims[5], int64_t n_planes, const uint64_t* pcg_state,
+                             const double* tab_s, const double* tab_t, const double* disc_r2, void* stream);
+
 /* The launch plan the kernel would use, as a JSON object in `buf` (for
  * tests, tuning and DESIGN.md).  Uses the current device's properties, or
  * B200 defaults (148 SMs, 227 KB smem/CTA) when no GPU is present. */
@@ -186,7 +223,7 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
  * reference transform.py:126 / 153 allocate them with np.zeros / np.empty):
  * D2H lands in them at full PCIe speed with no staging copy.  Freed blocks
  * stay cached for reuse (pinning is the expensive part, ~0.5 s per GB) up
- * to LFBP_PIN_CACHE_MB (default 16384) bytes; lfbp_host_cache_release
+ * to LFBP_PIN_CACHE_MB (default 8192) bytes; lfbp_host_cache_release
  * returns the cached blocks to the system. */
 int lfbp_host_alloc(int64_t bytes, void** out);
 int lfbp_host_free(void* p);

@@ -44,7 +44,7 @@ import numpy as np
 __all__ = [
     "slice_index", "wrap_phase", "target_cell", "mirror_index",
     "phase_pair_table", "source_pixels", "dropped_source_count",
-    "hprime_oracle", "closed_form_hprime", "EvenPixelDimsOracle",
+    "hprime_oracle", "hprime_oracle_split", "closed_form_hprime", "EvenPixelDimsOracle",
 ]
 
 
@@ -136,8 +136,12 @@ def _index_sets(shape):
     return S, T, X, Y
 
 
-def _gather_slab(src: np.ndarray, dst: np.ndarray, sets, inverse: bool) -> None:
+def _gather_slab(src: np.ndarray, dst: np.ndarray, sets, inverse: bool, y_range=None) -> None:
     S, T, X, Y = sets
+    if y_range is not None:                    # output columns y' in [y0, y1) only (forward)
+        y0, y1 = y_range
+        Y = Y[:, y0:y1]
+        dst = dst[..., y0:y1, :]
     sidx = (S[:, None, None, None], T[None, :, None, None],
             X[:, None, :, None], Y[None, :, None, :])
     if inverse:
@@ -173,6 +177,26 @@ def hprime_oracle(H: np.ndarray, inverse: bool = False, threads: int = 1) -> np.
     with _cf.ThreadPoolExecutor(threads) as pool:
         futs = [pool.submit(_gather_slab, H[..., a:b], out[..., a:b], sets, inverse)
                 for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+        for f in futs:
+            f.result()
+    return out
+
+
+def hprime_oracle_split(H: np.ndarray, threads: int) -> np.ndarray:
+    """Forward H' with the work split over ``threads`` host threads by depth
+    plane AND output column y' (each H'[..., y', z] is an independent gather),
+    so a sample of fewer planes than threads still uses every thread.  Same
+    result as ``hprime_oracle(H)``."""
+    H = np.asarray(H)
+    shape = tuple(int(v) for v in H.shape)
+    sets = _index_sets(shape)
+    out = np.zeros(shape, dtype=H.dtype, order="F")
+    n_y, n_z = shape[3], shape[4]
+    per_z = max(1, min(n_y, -(-int(threads) // n_z)))
+    tasks = [(z, (n_y * k) // per_z, (n_y * (k + 1)) // per_z) for z in range(n_z) for k in range(per_z)]
+    with _cf.ThreadPoolExecutor(max(1, int(threads))) as pool:
+        futs = [pool.submit(_gather_slab, H[..., z:z + 1], out[..., z:z + 1], sets, False, (y0, y1))
+                for z, y0, y1 in tasks if y1 > y0]
         for f in futs:
             f.result()
     return out

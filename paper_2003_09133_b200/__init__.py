@@ -11,7 +11,7 @@ from .arrays import BackprojArray, Dims5, PsfArray
 from .errors import (DimMismatch, DimsError, EvenPixelDims, FormatError, InvalidDims, IoError, LfbpError,
                      NativeError, NonFiniteInput, VerificationFailure)
 from .transform import (compute_backprojection, compute_psf_from_backprojection, dropped_source_count,
-                        f_order_empty, hprime_device, plan)
+                        f_order_empty, hprime_device, plan, plan_candidates, tune)
 
 __version__ = "0.1.0"
 
@@ -19,5 +19,5 @@ __all__ = [
     "BackprojArray", "Dims5", "PsfArray", "DimMismatch", "DimsError", "EvenPixelDims", "FormatError",
     "InvalidDims", "IoError", "LfbpError", "NativeError", "NonFiniteInput",
     "VerificationFailure", "compute_backprojection", "compute_psf_from_backprojection",
-    "dropped_source_count", "f_order_empty", "hprime_device", "plan",
+    "dropped_source_count", "f_order_empty", "hprime_device", "plan", "plan_candidates", "tune",
 ]

@@ -29,7 +29,8 @@ EXPORTS = (
     "lfbp_lf5_store_device", "lfbp_forward_project_device", "lfbp_backproject_device",
     "lfbp_safe_divide_device", "lfbp_forward_project2_device", "lfbp_max_device",
     "lfbp_safe_divide_peak_device", "lfbp_rl_update_device", "lfbp_host_alloc", "lfbp_host_free",
-    "lfbp_host_cache_release",
+    "lfbp_host_cache_release", "lfbp_tune", "lfbp_plan_candidates", "lfbp_host_copy",
+    "lfbp_synth_planes_device",
 )
 
 _lock = threading.Lock()
@@ -78,6 +79,12 @@ _SIGS = {
     "lfbp_host_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
     "lfbp_host_free": (ctypes.c_int, [ctypes.c_void_p]),
     "lfbp_host_cache_release": (ctypes.c_int, []),
+    "lfbp_tune": (ctypes.c_int, [_i64p, ctypes.c_int, ctypes.c_int, ctypes.c_int64]),
+    "lfbp_plan_candidates": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int]),
+    "lfbp_host_copy": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]),
+    "lfbp_synth_planes_device": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _i64p, ctypes.c_int64,
+                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                                 ctypes.c_void_p]),
     "lfbp_launch_count": (ctypes.c_int64, []),
     "lfbp_last_error": (ctypes.c_char_p, []),
     "lfbp_version": (ctypes.c_char_p, []),

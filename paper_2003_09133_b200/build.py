@@ -17,7 +17,8 @@ LIB = os.path.join(PKG, "libhprime.so")
 SOURCES = [os.path.join(CSRC, "lfbp_capi.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("hprime_kernel.cuh", "hprime_plan.h", "plane_sums.cuh",
                                                  "lf5_stream.inc", "projector.cuh",
-                                                 "host_pipeline.inc", "verify_capi.inc", "projector_capi.inc")] + [
+                                                 "host_pipeline.inc", "verify_capi.inc", "projector_capi.inc",
+                                                 "synth.cuh")] + [
     os.path.join(ROOT, "include", "lfbp_hprime.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -184,6 +184,9 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
       // element k of run x lives at R0 + x*row_pitch + k*E (see hprime_plan.h);
       // its 16-byte aligned superset starts (b & 15) bytes earlier
       uint8_t* dst = stage + kHdrBytes + 16 + (b0 & 15) + static_cast<int64_t>(x) * p.row_pitch - (b & 15);
+#if defined(HP_DBG_NOLOAD)  // pattern probe build: no reads of H
+      a_hi = a_lo;
+#endif
       if (a_hi > a_lo) {
         const uint32_t n = static_cast<uint32_t>(a_hi - a_lo);
         if (p.flags & HP_FLAG_LOAD_EVICT_FIRST)
@@ -259,6 +262,11 @@ template <int E, bool WRAP1>
 __device__ __forceinline__ void load_group(typename Word<E>::T* v, uint32_t a0, uint32_t x0, int32_t n_x,
                                            int32_t step, int32_t nr) {
   constexpr int VE = 16 / E;
+#if defined(HP_DBG_NOLDS)  // pattern probe build: no shared-memory reads
+#pragma unroll
+  for (int q = 0; q < VE; ++q) v[q] = a0 + q;
+  return;
+#endif
   if constexpr (WRAP1) {
     const int32_t d = n_x - static_cast<int32_t>(x0);   // elements before the wrap
     const uint32_t aw = a0 - nr;
@@ -347,6 +355,9 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
                                              uint32_t stage_s, int cw, int nc, int lane) {
   using T = typename Word<E>::T;
   constexpr int VE = 16 / E;
+#if defined(HP_DBG_NOSTORE)  // pattern probe build: bulk reads only
+  return;
+#endif
   const UnitHdr h = *reinterpret_cast<const UnitHdr*>(stage);
   const int32_t n_x = static_cast<int32_t>(p.n_x);
   const int32_t n_s = static_cast<int32_t>(p.n_s);

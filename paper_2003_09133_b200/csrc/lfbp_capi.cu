@@ -10,6 +10,7 @@
 //   lf5_stream.inc      LF5 file streaming (K4 value check)
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <atomic>
@@ -31,6 +32,7 @@
 #include "hprime_plan.h"
 #include "plane_sums.cuh"
 #include "projector.cuh"
+#include "synth.cuh"
 
 namespace {
 
@@ -571,6 +573,104 @@ int lfbp_hprime_multi(const void* src, void* dst, const int64_t dims[5], int dty
   return LFBP_OK;
 }
 
+int lfbp_tune(const int64_t dims[5], int dtype, int device, int64_t z_count) {
+  int rc = check_common(dims, dtype, 0);
+  if (rc) return rc;
+  const int E = elem_size(dtype);
+  if (z_count <= 0 || z_count > dims[4]) z_count = dims[4];
+  const int64_t pb = plane_elems(dims) * E;
+  // the two launch sizes a caller meets: z_count planes on the device API,
+  // and one chunk of the host pipeline (lfbp_hprime_host / _multi / LF5)
+  const int64_t jobs[2] = {z_count, host_chunk_planes(pb, dims[4])};
+  int cur = 0;
+  cudaGetDevice(&cur);
+  HP_CUDA(cudaSetDevice(device));
+  struct Restore {
+    int dev;
+    ~Restore() { cudaSetDevice(dev); }
+  } restore{cur};
+  for (int64_t planes : jobs) {
+    const int cls = tune_class(2 * planes * pb);
+    Knobs kn;
+    const TuneKey key{dims[0], dims[1], dims[2], dims[3], E, device, cls};
+    if (cls < 0 || tuned_knobs(key, kn)) continue;
+    // scratch of at most ~4 GB per array (the size class, not the plane
+    // count, selects the candidates; a few planes time them faithfully)
+    int64_t pt = std::min<int64_t>(planes, std::max<int64_t>(1, (int64_t(4) << 30) / pb));
+    while (pt < planes && tune_class(2 * pt * pb) != cls) ++pt;
+    const int64_t bytes = pt * pb;
+    struct Scratch {
+      void* a = nullptr;
+      void* b = nullptr;
+      cudaStream_t s = nullptr;
+      ~Scratch() {
+        if (s) cudaStreamSynchronize(s), cudaStreamDestroy(s);
+        if (a) cudaFree(a);
+        if (b) cudaFree(b);
+      }
+    } sc;
+    HP_CUDA(cudaMalloc(&sc.a, size_t(bytes) + 16));
+    HP_CUDA(cudaMalloc(&sc.b, size_t(bytes) + 16));
+    HP_CUDA(cudaMemset(sc.a, 0, size_t(bytes)));
+    HP_CUDA(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
+    const int64_t td[5] = {dims[0], dims[1], dims[2], dims[3], pt};
+    rc = autotune(key, sc.a, sc.b, td, E, 0, pt, bytes, sc.s, kn);
+    if (rc) return rc;
+  }
+  return LFBP_OK;
+}
+
+int lfbp_plan_candidates(int size_class, int32_t* knobs, int max_n) {
+  const Knobs* cand = size_class == 1 ? kCandidates : kSmallCandidates;
+  const int n = size_class == 1 ? kNumCandidates : kNumSmallCandidates;
+  if (size_class != 0 && size_class != 1) return -fail(LFBP_ERR_ARGUMENT, "size class must be 0 or 1");
+  for (int c = 0; c < n && c < max_n && knobs; ++c) {
+    knobs[4 * c + 0] = cand[c].stages;
+    knobs[4 * c + 1] = cand[c].stage_kb;
+    knobs[4 * c + 2] = cand[c].cwarps;
+    knobs[4 * c + 3] = cand[c].subwarp;
+  }
+  return n;
+}
+
+int lfbp_host_copy(void* dst, const void* src, int64_t bytes, int threads) {
+  if (bytes < 0 || (bytes && (!dst || !src))) return fail(LFBP_ERR_ARGUMENT, "bad host_copy arguments");
+  if (threads <= 0) {
+    copy_pool().copy(dst, src, size_t(bytes));
+  } else {
+    HostPool pool(threads);
+    pool.copy(dst, src, size_t(bytes));
+  }
+  return LFBP_OK;
+}
+
+int lfbp_synth_planes_device(void* dst, int dtype, const int64_t dims[5], int64_t n_planes, const uint64_t* pcg_state,
+                             const double* tab_s, const double* tab_t, const double* disc_r2, void* stream) {
+  if (!dims || !dst || !pcg_state || !tab_s || !tab_t) return fail(LFBP_ERR_ARGUMENT, "null argument");
+  if (!hp_dims_valid(dims[0], dims[1], dims[2], dims[3], n_planes > 0 ? n_planes : 1))
+    return fail(LFBP_ERR_INVALID_DIMS, "invalid dims");
+  const int E = elem_size(dtype);
+  if (!E) return fail(LFBP_ERR_ARGUMENT, "dtype code %d is not 1 (f32) or 2 (f64)", dtype);
+  if (n_planes <= 0) return LFBP_OK;
+  if (n_planes > 65535) return fail(LFBP_ERR_UNSUPPORTED, "at most 65535 planes per call");
+  const int64_t P = plane_elems(dims);
+  const int64_t per_block = int64_t(256 / 32) * 32 * hp::kSynthPer;
+  const int64_t bx = (P + per_block - 1) / per_block;
+  if (bx >= (int64_t(1) << 31)) return fail(LFBP_ERR_UNSUPPORTED, "plane too large");
+  const dim3 grid{unsigned(bx), unsigned(n_planes), 1u};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const hp::SynthPlane* pl = reinterpret_cast<const hp::SynthPlane*>(pcg_state);
+  if (E == 4)
+    hp::synth_kernel<float><<<grid, 256, 0, st>>>(static_cast<float*>(dst), dims[0], dims[1], dims[2], dims[3], pl,
+                                                  tab_s, tab_t, disc_r2);
+  else
+    hp::synth_kernel<double><<<grid, 256, 0, st>>>(static_cast<double*>(dst), dims[0], dims[1], dims[2], dims[3], pl,
+                                                   tab_s, tab_t, disc_r2);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  HP_CUDA(cudaGetLastError());
+  return LFBP_OK;
+}
+
 int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len) {
   int rc = check_common(dims, dtype, 0);
   if (rc) return rc;
@@ -611,74 +711,104 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
 #include "projector_capi.inc"
 
 // ---- pinned host blocks with a size-matched free cache ----
+// Blocks of at least LFBP_PIN_MMAP_MB (default 1024) are anonymous mappings
+// with transparent huge pages, first touched by the staging thread pool in
+// parallel and then registered (cudaHostRegister); smaller ones come from
+// cudaHostAlloc.  Registering pre-faulted huge pages avoids the driver's
+// single-threaded fault-and-pin walk over 4 KB pages.
 namespace {
+struct PinBlock {
+  int64_t cap;
+  bool mapped;  // mmap + cudaHostRegister (else cudaHostAlloc)
+};
 std::mutex g_pin_mu;
-std::map<void*, int64_t> g_pin_live;            // block -> capacity
-std::multimap<int64_t, void*> g_pin_cache;      // capacity -> free block
+std::map<void*, PinBlock> g_pin_live;           // block -> capacity, kind
+std::multimap<int64_t, std::pair<void*, bool>> g_pin_cache;  // capacity -> free block
 int64_t g_pin_cached = 0;
+
+void pin_release(void* p, bool mapped, int64_t cap) {
+  if (mapped) {
+    cudaHostUnregister(p);
+    munmap(p, size_t(cap));
+  } else {
+    cudaFreeHost(p);
+  }
+  cudaGetLastError();
+}
 }  // namespace
 
 int lfbp_host_alloc(int64_t bytes, void** out) {
   if (!out || bytes < 0) return fail(LFBP_ERR_ARGUMENT, "bad host_alloc arguments");
   *out = nullptr;
-  const int64_t want = std::max<int64_t>(bytes, 1);
+  int64_t want = std::max<int64_t>(bytes, 1);
+  const bool map = want >= (int64_t(env_int("LFBP_PIN_MMAP_MB", 1024)) << 20);
+  if (map) want = round_up(want, int64_t(2) << 20);
   {
     std::lock_guard<std::mutex> lk(g_pin_mu);
     // smallest cached block that fits and wastes at most a quarter of it
     auto it = g_pin_cache.lower_bound(want);
     if (it != g_pin_cache.end() && it->first - want <= it->first / 4) {
-      *out = it->second;
-      g_pin_live[it->second] = it->first;
+      *out = it->second.first;
+      g_pin_live[it->second.first] = PinBlock{it->first, it->second.second};
       g_pin_cached -= it->first;
       g_pin_cache.erase(it);
       return LFBP_OK;
     }
   }
   void* p = nullptr;
-  cudaError_t e = cudaHostAlloc(&p, size_t(want), cudaHostAllocPortable);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(LFBP_ERR_CUDA, "cudaHostAlloc(%lld): %s", (long long)want, cudaGetErrorString(e));
+  if (map) {
+    p = mmap(nullptr, size_t(want), PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return fail(LFBP_ERR_CUDA, "mmap(%lld): %s", (long long)want, strerror(errno));
+    madvise(p, size_t(want), MADV_HUGEPAGE);
+    uint8_t* b = static_cast<uint8_t*>(p);
+    copy_pool().for_range(size_t(want), size_t(2) << 20, [&](size_t a, size_t e) { memset(b + a, 0, e - a); });
+    cudaError_t e = cudaHostRegister(p, size_t(want), cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      munmap(p, size_t(want));
+      return fail(LFBP_ERR_CUDA, "cudaHostRegister(%lld): %s", (long long)want, cudaGetErrorString(e));
+    }
+  } else {
+    cudaError_t e = cudaHostAlloc(&p, size_t(want), cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LFBP_ERR_CUDA, "cudaHostAlloc(%lld): %s", (long long)want, cudaGetErrorString(e));
+    }
   }
   std::lock_guard<std::mutex> lk(g_pin_mu);
-  g_pin_live[p] = want;
+  g_pin_live[p] = PinBlock{want, map};
   *out = p;
   return LFBP_OK;
 }
 
 int lfbp_host_free(void* p) {
   if (!p) return LFBP_OK;
-  int64_t cap;
+  PinBlock blk;
   {
     std::lock_guard<std::mutex> lk(g_pin_mu);
     auto it = g_pin_live.find(p);
     if (it == g_pin_live.end()) return fail(LFBP_ERR_ARGUMENT, "pointer was not allocated by lfbp_host_alloc");
-    cap = it->second;
+    blk = it->second;
     g_pin_live.erase(it);
-    const int64_t limit = int64_t(env_int("LFBP_PIN_CACHE_MB", 16384)) << 20;
-    if (g_pin_cached + cap <= limit) {
-      g_pin_cache.emplace(cap, p);
-      g_pin_cached += cap;
+    const int64_t limit = int64_t(env_int("LFBP_PIN_CACHE_MB", 8192)) << 20;
+    if (g_pin_cached + blk.cap <= limit) {
+      g_pin_cache.emplace(blk.cap, std::make_pair(p, blk.mapped));
+      g_pin_cached += blk.cap;
       return LFBP_OK;
     }
   }
-  cudaError_t e = cudaFreeHost(p);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return fail(LFBP_ERR_CUDA, "cudaFreeHost: %s", cudaGetErrorString(e));
-  }
+  pin_release(p, blk.mapped, blk.cap);
   return LFBP_OK;
 }
 
 int lfbp_host_cache_release(void) {
-  std::multimap<int64_t, void*> blocks;
+  std::multimap<int64_t, std::pair<void*, bool>> blocks;
   {
     std::lock_guard<std::mutex> lk(g_pin_mu);
     blocks.swap(g_pin_cache);
     g_pin_cached = 0;
   }
-  for (auto& kv : blocks) cudaFreeHost(kv.second);
-  cudaGetLastError();
+  for (auto& kv : blocks) pin_release(kv.second.first, kv.second.second, kv.first);
   return LFBP_OK;
 }
 

@@ -35,7 +35,7 @@ import numpy as np
 
 from . import _native
 from .arrays import BackprojArray, PsfArray
-from .errors import EvenPixelDims, InvalidDims
+from .errors import EvenPixelDims, InvalidDims, NativeError
 
 log = logging.getLogger(__name__)
 
@@ -74,12 +74,31 @@ def _host_flags() -> int:
     return {"stage": _native.HOST_STAGE, "register": _native.HOST_REGISTER, "driver": 0}.get(mode, _native.HOST_STAGE)
 
 
-def _out_pinned() -> bool:
+def _out_pinned(nbytes: int) -> bool:
     """Where the drop-in's fresh result array lives (LFBP_OUT_MODE): "pinned"
     (default: a page-locked block from the library's cached host allocator,
     so the D2H lands directly) or "pageable" (plain numpy; the D2H is staged
-    through the pipeline's pinned chunks)."""
-    return os.environ.get("LFBP_OUT_MODE", "pinned") == "pinned"
+    through the pipeline's pinned chunks).  Results above LFBP_PIN_MAX_MB
+    (default 4096) are pageable: page-locking costs about 0.5 s/GB and a
+    71 GB block (C5) would take most of a 200 GB host out of the pageable
+    pool."""
+    if os.environ.get("LFBP_OUT_MODE", "pinned") != "pinned":
+        return False
+    return nbytes <= int(os.environ.get("LFBP_PIN_MAX_MB", "4096")) << 20
+
+
+def _result_array(shape, dtype) -> np.ndarray:
+    """The drop-in's fresh F-ordered result: pinned when small enough, and
+    pageable when page-locked memory is refused (the reference's plain
+    ``np.zeros`` never fails for lack of pinnable memory, so neither may
+    this)."""
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    if _out_pinned(nbytes):
+        try:
+            return _pinned_empty(shape, dtype)
+        except NativeError as e:
+            log.debug("pinned result of %d bytes refused (%s); using pageable memory", nbytes, e)
+    return np.empty(shape, dtype=dtype, order="F")
 
 
 class _PinnedBlock:
@@ -125,7 +144,7 @@ def _rearrange_host(data: np.ndarray, dims, inverse: bool, errs, device: int = 0
     if inverse and (shape[0] % 2 == 0 or shape[1] % 2 == 0):
         raise even(f"inverse undefined for even pixel dims (n_s, n_t)=({shape[0]}, {shape[1]}): "
                    "the forward mapping drops elements")
-    out = _pinned_empty(shape, src.dtype) if _out_pinned() else np.empty(shape, dtype=src.dtype, order="F")
+    out = _result_array(shape, src.dtype)
     rc = _native.lib().lfbp_hprime_host(src.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p),
                                         dvec, code, int(inverse), int(device), _host_flags())
     _native.check(rc, invalid, even)
@@ -253,3 +272,26 @@ def plan(shape, dtype=np.float32) -> dict:
     code = _DTYPE_CODE[np.dtype(dtype)]
     _native.check(_native.lib().lfbp_plan_json(_native.dims_array(shape), code, buf, len(buf)))
     return json.loads(buf.value.decode())
+
+
+def plan_candidates(size_class: int = 1) -> list:
+    """The autotuner's candidate plans, as (stages, stage_kb, consumer_warps,
+    lanes_per_row) tuples: size class 1 for launches moving >= 256 MB, 0 for
+    8-256 MB (``lfbp_plan_candidates``; no GPU needed)."""
+    lib = _native.lib()
+    n = lib.lfbp_plan_candidates(int(size_class), None, 0)
+    if n < 0:
+        _native.check(-n)
+    buf = (ctypes.c_int32 * (4 * n))()
+    lib.lfbp_plan_candidates(int(size_class), buf, n)
+    return [tuple(buf[4 * c:4 * c + 4]) for c in range(n)]
+
+
+def tune(shape, dtype=np.float32, device: int = 0, z_count: int = 0) -> dict:
+    """Tune the kernel plan for ``shape`` ahead of time on library-owned
+    scratch buffers (``lfbp_tune``): for launches of ``z_count`` planes
+    (0: all) and for the host pipeline's chunks.  Afterwards
+    ``hprime_device`` never synchronises.  Returns the tuned plan."""
+    code = _DTYPE_CODE[np.dtype(dtype)]
+    _native.check(_native.lib().lfbp_tune(_native.dims_array(shape), code, int(device), int(z_count)))
+    return plan(shape, dtype)

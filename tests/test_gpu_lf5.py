@@ -45,6 +45,33 @@ def test_transform_file_matches_reference_files(golden_small, golden_lf5, tmp_pa
             assert sha(back) == want["in_sha256"]
 
 
+def test_transform_file_in_place(golden_small, golden_lf5, tmp_path):
+    """`transform f f` works like the reference CLI (it loads the whole file
+    before saving): the result replaces the input only once it is complete,
+    and no temporary is left behind.  A failing in-place call (negative
+    values) leaves the input byte for byte."""
+    _torch()
+    import os
+
+    from paper_2003_09133_b200 import Dims5, InvalidDims, PsfArray, lf5
+    cases, arrays = golden_small
+    for name, want in list(golden_lf5.items())[:4]:
+        H = arrays[name + "__H"]
+        f = tmp_path / f"{name}.lf5"
+        lf5.save(PsfArray(Dims5(*H.shape), H), f)
+        lf5.transform_file(f, f)
+        assert sha(f) == want["out_sha256"], name
+    assert all(not n.startswith(".") and "lfbp-tmp" not in n for n in os.listdir(tmp_path))
+    neg = np.asfortranarray(-np.ones((5, 5, 3, 3, 2), dtype=np.float32))
+    g = tmp_path / "neg.lf5"
+    lf5.save(neg, g)
+    before = sha(g)
+    with pytest.raises(InvalidDims):
+        lf5.transform_file(g, g)
+    assert sha(g) == before
+    assert not any("lfbp-tmp" in n for n in os.listdir(tmp_path))
+
+
 def test_transform_file_errors(tmp_path):
     _torch()
     from paper_2003_09133_b200 import EvenPixelDims, InvalidDims, lf5

@@ -243,7 +243,13 @@ def test_rl_sharded_world_one_equals_rl_run(proj):
 
 
 @pytest.mark.parametrize("shape,img", [((15, 13, 5, 3, 2), (40, 33)), ((8, 12, 7, 3, 2), (20, 17)),
-                                       ((20, 18, 5, 7, 3), (33, 41)), ((33, 31, 11, 3, 2), (70, 23))])
+                                       ((20, 18, 5, 7, 3), (33, 41)), ((33, 31, 11, 3, 2), (70, 23)),
+                                       # tap classes of N = 17, 21, 31 taps (ceil(n_s / n_x)): the
+                                       # multi-block register window + remainder path that the C3/C4
+                                       # (N = 21, RL = 7) and C5 (N = 31, RL = 10) geometries take
+                                       ((51, 51, 3, 3, 2), (40, 37)), ((85, 83, 5, 5, 2), (47, 44)),
+                                       ((63, 63, 3, 3, 2), (45, 41)), ((62, 60, 3, 3, 2), (44, 39)),
+                                       ((93, 93, 3, 3, 2), (50, 47)), ((93, 91, 3, 3, 1), (101, 37))])
 def test_both_polyphase_forms_match_oracle(shape, img):
     """Every device form against the oracle, odd and even sizes: the H form
     of the forward projection and the H'-stamp backprojection run as

@@ -91,3 +91,24 @@ def test_cli_plan_and_errors(tmp_path, capsys):
     assert '"J"' in capsys.readouterr().out
     assert main(["transform", str(tmp_path / "missing.lf5"), str(tmp_path / "o.lf5")]) == 2
     assert "IoError" in capsys.readouterr().err
+
+
+def test_failed_in_place_transform_leaves_the_input_intact(tmp_path):
+    """transform_file(f, f) writes to a temporary next to f and renames it
+    only on success: when the transform fails (here: no GPU, or any device
+    error) the input file is neither truncated nor deleted, and no temporary
+    is left behind."""
+    import os
+
+    import torch
+    d = Dims5(9, 7, 3, 5, 2)
+    H = np.asfortranarray(np.random.default_rng(3).random(d.shape).astype(np.float32))
+    p = tmp_path / "h.lf5"
+    lf5.save(PsfArray(d, H), p)
+    before = sha(p)
+    if torch.cuda.is_available():
+        pytest.skip("exercises the failure path; the GPU test covers the successful in-place transform")
+    with pytest.raises(Exception):
+        lf5.transform_file(p, p)
+    assert sha(p) == before
+    assert sorted(os.listdir(tmp_path)) == ["h.lf5"]

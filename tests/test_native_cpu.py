@@ -173,3 +173,27 @@ def test_header_is_plain_c_and_the_abi_runs_from_c(tmp_path):
     r = subprocess.run([_build_c_example(tmp_path), "--abi"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert "abi ok" in r.stdout
+
+
+@pytest.mark.parametrize("threads", [1, 3, 12, 16])
+@pytest.mark.parametrize("nbytes", [34_692_100, (4 << 20) + 4, (64 << 20) + 1, 12 * 64 * 100_003 + 4])
+def test_host_copy_covers_every_byte(threads, nbytes):
+    """The staging memcpy pool splits [0, n) over its workers: every byte is
+    copied whatever n mod workers is.  34,692,100 B is one (155,155,19,19) f32
+    plane -- with 12 workers the former split (floor(n/parts) rounded to 64)
+    left its last 4 bytes uncopied."""
+    src = np.frombuffer(np.random.default_rng(nbytes % 1000).bytes(nbytes), dtype=np.uint8)
+    dst = np.zeros(nbytes, dtype=np.uint8)
+    rc = _native.lib().lfbp_host_copy(dst.ctypes.data_as(ctypes.c_void_p), src.ctypes.data_as(ctypes.c_void_p),
+                                      nbytes, threads)
+    assert rc == _native.OK
+    assert np.array_equal(dst, src)
+
+
+def test_plan_candidates_are_exported():
+    from paper_2003_09133_b200 import plan_candidates
+    large, small = plan_candidates(1), plan_candidates(0)
+    assert len(large) >= 8 and len(small) >= 4
+    assert all(len(k) == 4 and k[0] >= 1 and k[1] >= 1 and k[2] >= 1 for k in large + small)
+    assert len(set(large)) == len(large)
+    assert _native.lib().lfbp_plan_candidates(7, None, 0) < 0
