@@ -102,9 +102,11 @@ int lfbp_hprime_host(const void* src, void* dst, const int64_t dims[5], int dtyp
 int lfbp_tune(const int64_t dims[5], int dtype, int device, int64_t z_count);
 
 /* The autotuner's candidate plans for size class 1 (launches moving
- * >= 256 MB) or 0 (8-256 MB): writes up to `max_n` records of 4 int32
- * (smem stages, stage KB, consumer warps, lanes per row; 0 = by row length)
- * into `knobs` (may be NULL) and returns the number of candidates.  No GPU. */
+ * >= 256 MB) or 0 (8-256 MB): writes up to `max_n` records of 6 int32
+ * (smem stages, stage KB, consumer warps, lanes per row -- 0 = by row
+ * length --, unit-order flags -- 8 = along y' diagonals, 16 = rotated run /
+ * row order --, SMs used -- 0 = all) into `knobs` (may be NULL) and returns
+ * the number of candidates.  No GPU. */
 int lfbp_plan_candidates(int size_class, int32_t* knobs, int max_n);
 
 /* memcpy of `bytes` split over `threads` host threads (<= 0: the library's

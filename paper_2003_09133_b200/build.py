@@ -1,8 +1,10 @@
-"""In-tree build of the CUDA library (nvcc, sm_100a) and of the C oracle port.
+"""In-tree build of the CUDA library (nvcc, sm_100a).
 
 ``python -m paper_2003_09133_b200.build`` or ``__graft_entry__.build()``.
 The output ``paper_2003_09133_b200/libhprime.so`` is git-ignored but travels
-with the repo snapshot to the GPU box.
+with the repo snapshot to the GPU box.  The oracle (``oracle/``) is numpy
+test infrastructure: the reference is pure Python, so there is no C oracle
+or compiled reference (``oracle/_ref``) to build.
 """
 from __future__ import annotations
 

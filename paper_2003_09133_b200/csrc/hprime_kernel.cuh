@@ -84,6 +84,7 @@ struct UnitHdr {
   long long plane_off;  // z * plane_elems
   int32_t y, t0, jb, i_lo, i_hi, s_lo, o0;
   int32_t next_row;     // work counter: consumer warps claim rows with atomicAdd
+  int32_t rot;          // HP_FLAG_ROTATE: rows are claimed starting at this one
 };
 constexpr int kHdrBytes = 64;
 
@@ -100,7 +101,23 @@ __device__ __forceinline__ Unit decode_unit(const HpPlan& p, uint32_t u) {
   Unit w;
   int32_t band;
   uint32_t r2;
-  if (p.flags & HP_FLAG_BAND_FASTEST) {  // consecutive units read adjacent t-bands
+  if (p.flags & HP_FLAG_DIAGONAL) {
+    // blocks of tile_y diagonals y' = (y + t0 - c_t) mod n_y; inside a block
+    // the diagonal is fastest, then the band: a window of consecutive units
+    // writes runs of adjacent rows of few y' and reads runs of tile_y
+    // adjacent rows of each y
+    r2 = hp_div(p.zc_div, u);
+    const uint32_t r = u - r2 * p.zc_div.d;
+    const uint32_t db = hp_div(p.yblk_div, r);
+    const uint32_t rem = r - db * p.yblk_div.d;
+    const HpFastDiv& tdiv = (static_cast<int32_t>(db) == p.n_yblocks - 1) ? p.tyl_div : p.ty_div;
+    const uint32_t b = hp_div(tdiv, rem);
+    band = static_cast<int32_t>(b);
+    const uint32_t d = db * p.ty_div.d + (rem - b * tdiv.d);
+    const uint32_t tm = hp_mod(p.ny_div, static_cast<uint32_t>(band * p.J));
+    const uint32_t cm = hp_mod(p.ny_div, static_cast<uint32_t>(p.c_t));
+    w.y = hp_mod(p.ny_div, d + cm + p.ny_div.d - tm);
+  } else if (p.flags & HP_FLAG_BAND_FASTEST) {  // consecutive units read adjacent t-bands
     const uint32_t r = hp_div(p.nb_div, u);
     band = static_cast<int32_t>(u - r * p.nb_div.d);
     r2 = hp_div(p.ny_div, r);
@@ -176,7 +193,10 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
   const int64_t b0 = w.run_off0 * E;
   uint32_t tx = 0;
   if (run_bytes > 0) {
-    for (int32_t x = 32 * pw + lane; x < p.n_x; x += 32 * p.producers) {
+    const int32_t rot = (p.flags & HP_FLAG_ROTATE) ? static_cast<int32_t>(hp_mod(p.nx_div, u)) : 0;
+    for (int32_t xl = 32 * pw + lane; xl < p.n_x; xl += 32 * p.producers) {
+      // lanes issue in order; with HP_FLAG_ROTATE unit u starts at run u mod n_x
+      const int32_t x = xl + rot < p.n_x ? xl + rot : xl + rot - static_cast<int32_t>(p.n_x);
       const int64_t b = b0 + x * xstride;
       const int64_t a_lo = b & ~int64_t(15);
       int64_t a_hi = (b + run_bytes + 15) & ~int64_t(15);
@@ -211,6 +231,7 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
     h->s_lo = w.s_lo;
     h->o0 = static_cast<int32_t>(b0 & 15);
     h->next_row = 0;
+    h->rot = (p.flags & HP_FLAG_ROTATE) ? static_cast<int32_t>(u % static_cast<uint32_t>(w.jb * p.n_x)) : 0;
   }
   tx = __reduce_add_sync(0xffffffffu, tx);
   __syncwarp();                                    // header and tail stores before the release
@@ -232,10 +253,36 @@ __device__ __forceinline__ typename Word<E>::T lds(uint32_t addr) {
 
 template <int E>
 __device__ __forceinline__ void st_vec(typename Word<E>::T* dst, const typename Word<E>::T* v) {
+#if defined(HP_ST_VARIANT) && HP_ST_VARIANT == 1  // experiment builds: streaming-store hints
+  if constexpr (E == 4)
+    asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]) : "memory");
+  else
+    asm volatile("st.global.cs.v2.b64 [%0], {%1, %2};" ::"l"(dst), "l"(v[0]), "l"(v[1]) : "memory");
+#elif defined(HP_ST_VARIANT) && HP_ST_VARIANT == 2
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if constexpr (E == 4)
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "l"(pol) : "memory");
+  else
+    asm volatile("st.global.L2::cache_hint.v2.b64 [%0], {%1, %2}, %3;" ::"l"(dst), "l"(v[0]), "l"(v[1]), "l"(pol)
+                 : "memory");
+#elif defined(HP_ST_VARIANT) && HP_ST_VARIANT == 3
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  if constexpr (E == 4)
+    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "l"(pol) : "memory");
+  else
+    asm volatile("st.global.L2::cache_hint.v2.b64 [%0], {%1, %2}, %3;" ::"l"(dst), "l"(v[0]), "l"(v[1]), "l"(pol)
+                 : "memory");
+#else
   if constexpr (E == 4)
     st_v4(dst, v[0], v[1], v[2], v[3]);
   else
     st_v2_64(dst, v[0], v[1]);
+#endif
 }
 
 // Values of the VE elements of group g whose first element has source phase
@@ -386,9 +433,10 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
     const int32_t r0 = __shfl_sync(0xffffffffu, claim, 0);
     if (r0 >= rows) break;
     if (lane == 0) claim = atomicAdd(next_row, R);
-    const int32_t r = r0 + (lane >> lw);
+    const int32_t rc = r0 + (lane >> lw);
     do {  // this sub-warp's row (none past the end of the unit)
-    if (r >= rows) break;
+    if (rc >= rows) break;
+    const int32_t r = rc + h.rot < rows ? rc + h.rot : rc + h.rot - rows;
     const int32_t tl = static_cast<int32_t>(hp_div(p.nx_div, static_cast<uint32_t>(r)));
     const int32_t xp = r - tl * n_x;
     const int32_t t = h.t0 + tl;
@@ -455,7 +503,10 @@ __global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8
         mbar_wait(smem_u32(&empty[st]), ph ^ 1u);
         fence_proxy_async_smem();
       }
-      issue_unit<E>(p, src, first + k * stride, stages + static_cast<int64_t>(st) * p.stage_bytes,
+      uint32_t u = first + k * stride;
+      if (p.flags & HP_FLAG_SCRAMBLE)  // multiplicative permutation of the unit order
+        u = static_cast<uint32_t>((static_cast<uint64_t>(u) * p.scr_mul) % static_cast<uint64_t>(p.n_units));
+      issue_unit<E>(p, src, u, stages + static_cast<int64_t>(st) * p.stage_bytes,
                     smem_u32(&full[st]), lane, warp, policy);
       if (++st == S) {
         st = 0;

@@ -108,10 +108,14 @@ struct Knobs {
   int stage_kb = 48;   // target bytes of one staged unit (sets the t-band J)
   int cwarps = 12;     // consumer warps per CTA
   int subwarp = 0;     // lanes per output row; 0 = by row length
+  int flags = 0;       // HP_FLAG_* unit order (HP_FLAG_DIAGONAL, HP_FLAG_ROTATE)
+  int grid_sm = 0;     // SMs given a persistent CTA (0 = all): fewer requests in flight
 };
+constexpr int kKnobFields = 6;
 
 const char* const kKnobEnv[] = {"LFBP_STAGES", "LFBP_STAGE_KB", "LFBP_CONSUMER_WARPS", "LFBP_SUBWARP",
-                                "LFBP_CTAS_PER_SM", "LFBP_BAND", "LFBP_STAGE_MAX_KB"};
+                                "LFBP_CTAS_PER_SM", "LFBP_BAND", "LFBP_STAGE_MAX_KB", "LFBP_KFLAGS",
+                                "LFBP_GRID", "LFBP_TILE_Y"};
 
 bool env_knobs_set() {
   for (const char* n : kKnobEnv) {
@@ -143,6 +147,11 @@ const Knobs kCandidates[] = {
     {3, 48, 8, 8},  {4, 48, 12, 16}, {4, 48, 8, 8},  {4, 48, 8, 16}, {2, 96, 8, 16},
     {3, 64, 8, 32}, {4, 48, 16, 16}, {2, 96, 8, 8},  {4, 16, 8, 0},  {4, 16, 4, 4},
     {2, 96, 12, 32},  // C4 with the v7 loop: J = 3, +3 % over the former best (profiles/r01_sweep_v7.jsonl)
+    // long single-row units (C5): unit order along y' diagonals, rotated run /
+    // row order, and 140 of 148 SMs -- at full clock the 148-CTA y-fastest
+    // plan oversubscribes the memory system on some boxes (profiles/r02_*)
+    {3, 64, 8, 32, HP_FLAG_DIAGONAL}, {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ROTATE},
+    {3, 64, 8, 32, HP_FLAG_DIAGONAL, 140}, {3, 64, 8, 32, 0, 140}, {3, 64, 8, 32, HP_FLAG_ROTATE},
 };
 // Small problems (8-256 MB moved) are latency-bound: smaller stages (narrower
 // t-bands, several CTAs per SM) and short-row sub-warps; measured on the
@@ -231,6 +240,19 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   const int64_t units = z_count * p.n_chunks * int64_t(p.n_bands) * d[3];
   if (units >= (1ll << 31)) return fail(LFBP_ERR_UNSUPPORTED, "too many work units (%lld)", (long long)units);
   p.n_units = units;
+  {  // scramble multiplier: near 0.618 n_units, coprime to it
+    uint64_t m = std::max<uint64_t>(1, uint64_t(double(units) * 0.6180339887));
+    auto gcd = [](uint64_t a, uint64_t b) {
+      while (b) {
+        const uint64_t t = a % b;
+        a = b;
+        b = t;
+      }
+      return a;
+    };
+    while (units > 1 && gcd(m, uint64_t(units)) != 1) ++m;
+    p.scr_mul = static_cast<uint32_t>(units > 1 ? m % uint64_t(units) : 1);
+  }
   int per_sm = 0;
   if (dp.real) {
     cudaError_t e = (E == 4) ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hp::hprime_kernel<4>,
@@ -246,7 +268,9 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   if (per_sm < 1) return fail(LFBP_ERR_UNSUPPORTED, "kernel does not fit on an SM");
   p.ctas_per_sm = per_sm;
   p.grid = static_cast<int32_t>(std::min<int64_t>(units, int64_t(per_sm) * dp.sm_count));
-  p.flags = env_int("LFBP_KFLAGS", 0);
+  const int grid_cap = env_int("LFBP_GRID", kn.grid_sm);  // fewer persistent CTAs
+  if (grid_cap > 0) p.grid = std::min<int32_t>(p.grid, int32_t(int64_t(grid_cap) * per_sm));
+  p.flags = env_int("LFBP_KFLAGS", kn.flags);
   // lanes per output row: enough 16-byte groups per lane to amortise the row setup
   const int64_t groups = (std::min<int64_t>(p.C, d[0]) * E + 15) / 16 + 1;
   int W = env_int("LFBP_SUBWARP", kn.subwarp);
@@ -263,7 +287,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   // ((181,181,95,55): 0.74 -> 0.82 of copy; (307,307,51,51): 0.84 -> 0.86).
   // With n_x <= 32 (all BASELINE configs) plain y-fastest order measured best
   // (profiles/r01_order_probe.jsonl).
-  int ty = env_int("LFBP_TILE_Y", d[2] > 32 ? 4 : int(d[3]));
+  int ty = env_int("LFBP_TILE_Y", (p.flags & HP_FLAG_DIAGONAL) ? 1 : d[2] > 32 ? 4 : int(d[3]));
   ty = std::max<int>(1, std::min<int>(ty, int(d[3])));
   p.tile_y = ty;
   p.n_yblocks = static_cast<int32_t>((d[3] + ty - 1) / ty);
@@ -396,9 +420,10 @@ int autotune(const TuneKey& key, const void* src, void* dst, const int64_t dims[
     std::sort(v, v + kRounds - 1);
     const float med = v[(kRounds - 1) / 2];
     if (log)
-      fprintf(stderr, "[lfbp tune] (%lld,%lld,%lld,%lld) E=%d class=%d knobs {%d,%d,%d,%d}: %.4f ms\n",
+      fprintf(stderr, "[lfbp tune] (%lld,%lld,%lld,%lld) E=%d class=%d knobs {%d,%d,%d,%d,%d,%d}: %.4f ms\n",
               (long long)key.n_s, (long long)key.n_t, (long long)key.n_x, (long long)key.n_y, key.E, key.cls,
-              cand[c].stages, cand[c].stage_kb, cand[c].cwarps, cand[c].subwarp, med);
+              cand[c].stages, cand[c].stage_kb, cand[c].cwarps, cand[c].subwarp, cand[c].flags, cand[c].grid_sm,
+              med);
     if (med < best_ms) {
       best_ms = med;
       best = cand[c];
@@ -621,14 +646,17 @@ int lfbp_tune(const int64_t dims[5], int dtype, int device, int64_t z_count) {
 }
 
 int lfbp_plan_candidates(int size_class, int32_t* knobs, int max_n) {
+  if (size_class != 0 && size_class != 1) return -fail(LFBP_ERR_ARGUMENT, "size class must be 0 or 1");
   const Knobs* cand = size_class == 1 ? kCandidates : kSmallCandidates;
   const int n = size_class == 1 ? kNumCandidates : kNumSmallCandidates;
-  if (size_class != 0 && size_class != 1) return -fail(LFBP_ERR_ARGUMENT, "size class must be 0 or 1");
   for (int c = 0; c < n && c < max_n && knobs; ++c) {
-    knobs[4 * c + 0] = cand[c].stages;
-    knobs[4 * c + 1] = cand[c].stage_kb;
-    knobs[4 * c + 2] = cand[c].cwarps;
-    knobs[4 * c + 3] = cand[c].subwarp;
+    int32_t* k = knobs + kKnobFields * c;
+    k[0] = cand[c].stages;
+    k[1] = cand[c].stage_kb;
+    k[2] = cand[c].cwarps;
+    k[3] = cand[c].subwarp;
+    k[4] = cand[c].flags;
+    k[5] = cand[c].grid_sm;
   }
   return n;
 }
@@ -696,12 +724,14 @@ int lfbp_plan_json(const int64_t dims[5], int dtype, char* buf, int64_t buf_len)
                    "{\"elem\": %d, \"J\": %d, \"n_bands\": %d, \"C\": %d, \"n_chunks\": %d, \"row_pitch\": %d, "
                    "\"stage_bytes\": %d, \"stages\": %d, \"threads\": %d, \"smem_bytes\": %d, \"ctas_per_sm\": %d, "
                    "\"grid\": %d, \"n_units\": %lld, \"sub_width\": %d, \"sm_count\": %d, \"device_props\": \"%s\", "
-                   "\"producers\": %d, \"tile_y\": %d, \"autotuned\": %s, \"knobs\": [%d, %d, %d, %d]}",
+                   "\"producers\": %d, \"tile_y\": %d, \"flags\": %d, \"autotuned\": %s, "
+                   "\"knobs\": [%d, %d, %d, %d, %d, %d]}",
                    p.elem, p.J, p.n_bands, p.C, p.n_chunks, p.row_pitch, p.stage_bytes, p.stages, p.threads,
                    p.smem_bytes, p.ctas_per_sm, p.grid, (long long)p.n_units, p.sub_width, dp.sm_count,
-                   dp.real ? "queried" : "b200-defaults", p.producers, p.tile_y, tuned ? "true" : "false",
+                   dp.real ? "queried" : "b200-defaults", p.producers, p.tile_y, p.flags, tuned ? "true" : "false",
                    env_int("LFBP_STAGES", kn.stages), env_int("LFBP_STAGE_KB", kn.stage_kb),
-                   env_int("LFBP_CONSUMER_WARPS", kn.cwarps), env_int("LFBP_SUBWARP", kn.subwarp));
+                   env_int("LFBP_CONSUMER_WARPS", kn.cwarps), env_int("LFBP_SUBWARP", kn.subwarp),
+                   env_int("LFBP_KFLAGS", kn.flags), env_int("LFBP_GRID", kn.grid_sm));
   if (w < 0 || w >= buf_len) return fail(LFBP_ERR_ARGUMENT, "buffer too small");
   return LFBP_OK;
 }

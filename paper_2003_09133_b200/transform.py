@@ -276,15 +276,16 @@ def plan(shape, dtype=np.float32) -> dict:
 
 def plan_candidates(size_class: int = 1) -> list:
     """The autotuner's candidate plans, as (stages, stage_kb, consumer_warps,
-    lanes_per_row) tuples: size class 1 for launches moving >= 256 MB, 0 for
-    8-256 MB (``lfbp_plan_candidates``; no GPU needed)."""
+    lanes_per_row, order_flags, grid_sms) tuples: size class 1 for launches
+    moving >= 256 MB, 0 for 8-256 MB (``lfbp_plan_candidates``; no GPU
+    needed)."""
     lib = _native.lib()
     n = lib.lfbp_plan_candidates(int(size_class), None, 0)
     if n < 0:
         _native.check(-n)
-    buf = (ctypes.c_int32 * (4 * n))()
+    buf = (ctypes.c_int32 * (6 * n))()
     lib.lfbp_plan_candidates(int(size_class), buf, n)
-    return [tuple(buf[4 * c:4 * c + 4]) for c in range(n)]
+    return [tuple(buf[6 * c:6 * c + 6]) for c in range(n)]
 
 
 def tune(shape, dtype=np.float32, device: int = 0, z_count: int = 0) -> dict:

@@ -194,6 +194,6 @@ def test_plan_candidates_are_exported():
     from paper_2003_09133_b200 import plan_candidates
     large, small = plan_candidates(1), plan_candidates(0)
     assert len(large) >= 8 and len(small) >= 4
-    assert all(len(k) == 4 and k[0] >= 1 and k[1] >= 1 and k[2] >= 1 for k in large + small)
+    assert all(len(k) == 6 and k[0] >= 1 and k[1] >= 1 and k[2] >= 1 for k in large + small)
     assert len(set(large)) == len(large)
     assert _native.lib().lfbp_plan_candidates(7, None, 0) < 0
