@@ -464,7 +464,11 @@ def main():
         hout.free()
 
     shard_info = _gather_objects({"rank": rank, "planes": [z0, z1], "kernel_ms_avg": round(statistics.mean(kern_ms), 4)
-                                  if kern_ms and nz else 0.0, "verified": verified}, world)
+                                  if kern_ms and nz else 0.0, "verified": verified,
+                                  "e2e_verified": e2e["matches_reference_digests"] if e2e else None}, world)
+    if e2e is not None:
+        e2e["matches_reference_digests"] = _all_verified(
+            [{"planes": s["planes"], "verified": s["e2e_verified"]} for s in shard_info])
 
     cpu = cpu_port = None
     if rank == 0 and world == 1 and not args.no_cpu:

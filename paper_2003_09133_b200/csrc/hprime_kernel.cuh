@@ -472,7 +472,7 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
 // Warps 0..producers-1 produce, the rest consume; full/empty mbarrier ring
 // of `stages` buffers, so consumer warps never wait for each other.
 template <int E>
-__global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8_t* __restrict__ src,
+__global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const uint8_t* __restrict__ src,
                                                      uint8_t* __restrict__ dst) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -503,10 +503,7 @@ __global__ void __launch_bounds__(544) hprime_kernel(const HpPlan p, const uint8
         mbar_wait(smem_u32(&empty[st]), ph ^ 1u);
         fence_proxy_async_smem();
       }
-      uint32_t u = first + k * stride;
-      if (p.flags & HP_FLAG_SCRAMBLE)  // multiplicative permutation of the unit order
-        u = static_cast<uint32_t>((static_cast<uint64_t>(u) * p.scr_mul) % static_cast<uint64_t>(p.n_units));
-      issue_unit<E>(p, src, u, stages + static_cast<int64_t>(st) * p.stage_bytes,
+      issue_unit<E>(p, src, first + k * stride, stages + static_cast<int64_t>(st) * p.stage_bytes,
                     smem_u32(&full[st]), lane, warp, policy);
       if (++st == S) {
         st = 0;

@@ -67,7 +67,6 @@ HP_HD uint32_t hp_mod(const HpFastDiv& f, uint32_t n) {
 #define HP_FLAG_BAND_FASTEST 4      // unit order: t-band fastest instead of y
 #define HP_FLAG_DIAGONAL 8          // unit order: t-band fastest along a y' = y + t - c_t diagonal
 #define HP_FLAG_ROTATE 16           // unit u issues its runs / claims its rows starting at u mod n
-#define HP_FLAG_SCRAMBLE 32         // unit order permuted by u -> u * scr_mul mod n_units
 
 struct HpPlan {
   // geometry of the (chunk) arrays the kernel sees
@@ -96,7 +95,6 @@ struct HpPlan {
   int32_t gx_inc;             // (sub_width * 16/elem) mod n_x: phase advance of one stride
   int32_t producers;          // producer warps (warps 0..producers-1); they split a unit's n_x runs
   int64_t n_units;            // z_count * n_chunks * n_bands * n_y  (< 2^31)
-  uint32_t scr_mul;           // HP_FLAG_SCRAMBLE multiplier, coprime to n_units
   HpFastDiv nx_div;           // mod n_x on the element path
   HpFastDiv ny_div;           // unit decode / y' wrap
   HpFastDiv nb_div;           // unit decode: bands

@@ -240,19 +240,6 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   const int64_t units = z_count * p.n_chunks * int64_t(p.n_bands) * d[3];
   if (units >= (1ll << 31)) return fail(LFBP_ERR_UNSUPPORTED, "too many work units (%lld)", (long long)units);
   p.n_units = units;
-  {  // scramble multiplier: near 0.618 n_units, coprime to it
-    uint64_t m = std::max<uint64_t>(1, uint64_t(double(units) * 0.6180339887));
-    auto gcd = [](uint64_t a, uint64_t b) {
-      while (b) {
-        const uint64_t t = a % b;
-        a = b;
-        b = t;
-      }
-      return a;
-    };
-    while (units > 1 && gcd(m, uint64_t(units)) != 1) ++m;
-    p.scr_mul = static_cast<uint32_t>(units > 1 ? m % uint64_t(units) : 1);
-  }
   int per_sm = 0;
   if (dp.real) {
     cudaError_t e = (E == 4) ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hp::hprime_kernel<4>,

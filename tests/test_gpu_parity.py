@@ -180,6 +180,47 @@ def test_plan_variants_are_bit_exact(monkeypatch, env, shape, dtype):
     assert to_host(out).tobytes() == fbytes(hprime_oracle(H))
 
 
+ORDER_SHAPES = [
+    ((55, 55, 11, 11, 3), np.float32), ((195, 195, 15, 15, 2), np.float32), ((273, 273, 13, 13, 2), np.float64),
+    ((399, 399, 19, 19, 1), np.float32), ((631, 631, 21, 21, 1), np.float32), ((9, 9, 9, 9, 3), np.float32),
+    ((10, 12, 9, 3, 2), np.float64), ((64, 31, 17, 5, 2), np.float32), ((46, 40, 23, 7, 2), np.float32),
+    ((100, 51, 25, 5, 1), np.float64), ((55, 29, 27, 29, 1), np.float32), ((60, 33, 29, 3, 2), np.float64),
+    ((31, 31, 31, 31, 1), np.float32), ((33, 32, 31, 1, 2), np.float64), ((1001, 40, 31, 5, 2), np.float32),
+    ((28, 13, 13, 13, 2), np.float32), ((12, 14, 11, 3, 4), np.float32),
+    ((45, 29, 13, 7, 2), np.float32), ((33, 17, 33, 3, 1), np.float32), ((21, 41, 5, 9, 3), np.float32),
+    ((3, 3, 3, 3, 2), np.float32), ((51, 47, 3, 5, 2), np.float64), ((77, 5, 1, 1, 3), np.float32),
+]
+
+
+@pytest.mark.parametrize("env", [
+    {"LFBP_KFLAGS": "8"}, {"LFBP_KFLAGS": "24"}, {"LFBP_KFLAGS": "8", "LFBP_TILE_Y": "3"},
+    {"LFBP_KFLAGS": "16"}, {"LFBP_KFLAGS": "24", "LFBP_STAGE_MAX_KB": "2"},
+    {"LFBP_KFLAGS": "24", "LFBP_STAGE_KB": "200", "LFBP_STAGE_MAX_KB": "200"},
+    {"LFBP_KFLAGS": "8", "LFBP_GRID": "37", "LFBP_CONSUMER_WARPS": "3"}, {"LFBP_KFLAGS": "0", "LFBP_GRID": "140"},
+])
+@pytest.mark.parametrize("shape,dtype", ORDER_SHAPES)
+def test_unit_orders_are_bit_exact(monkeypatch, env, shape, dtype):
+    """The unit orders the autotuner can pick -- along y' diagonals (blocks
+    of diagonals), rotated run / row order -- and a reduced SM count write
+    the oracle's H' bit for bit on odd and even sizes, f32 and f64, bands
+    and i-chunks, and the inverse restores H."""
+    torch = _torch()
+    from paper_2003_09133_b200 import hprime_device, plan
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    p = plan(shape, dtype)
+    assert p["flags"] == int(env["LFBP_KFLAGS"])
+    H = random_psf_like_reference(shape, density=0.9, seed=sum(shape) + 3, dtype=dtype)
+    out = hprime_device(to_device(H))
+    torch.cuda.synchronize()
+    assert to_host(out).tobytes() == fbytes(hprime_oracle(H))
+    if shape[0] % 2 and shape[1] % 2:
+        back = hprime_device(out, inverse=True)
+        torch.cuda.synchronize()
+        assert to_host(back).tobytes() == fbytes(H)
+
+
 def test_z_range_writes_only_its_planes():
     torch = _torch()
     from paper_2003_09133_b200 import hprime_device

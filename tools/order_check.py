@@ -21,7 +21,7 @@ def main():
     ref = hprime_device(src)
     res = []
     for flags, ty in [("8", "1"), ("8", "2"), ("8", "3"), ("8", "4"), ("8", "7"), ("8", str(shape[3])), ("4", ""),
-                      ("0", "3"), ("16", ""), ("32", ""), ("48", ""), ("24", "1"), ("56", "2")]:
+                      ("0", "3"), ("16", ""), ("24", "1"), ("64", ""), ("72", "1"), ("80", "")]:
         os.environ["LFBP_KFLAGS"], os.environ["LFBP_TILE_Y"] = flags, ty
         out = hprime_device(src)
         n, _ = compare_device(out, ref)

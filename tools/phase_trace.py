@@ -30,7 +30,7 @@ def main():
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
     shape = tuple(int(v) for v in a.shape.split(","))
-    dt = torch.float64 if a.f64 else torch.float32
+    dt = torch.float64 if (a.f64 or os.environ.get("LFBP_PT_F64")) else torch.float32
     src = f_order_empty(shape, dt)
     src.permute(4, 3, 2, 1, 0).reshape(-1).uniform_()
     out = f_order_empty(shape, dt)
