@@ -31,8 +31,10 @@ Rank 0 prints one JSON line:
                of the same config (chunked: planes are independent);
                cpu_baseline_port: the oracle's numpy restatement on all host
                threads
-``--impl reference`` prints the same metric for the CPU arm alone (the
-oracle port, every host thread, a bounded plane sample of the same config).
+``--impl reference`` prints the same metric for the CPU arm alone: the
+unmodified reference (baseline/_ref) on a bounded plane sample of the same
+config, one process per plane on every host thread (the oracle port when the
+reference is not installed).
 """
 from __future__ import annotations
 
@@ -54,7 +56,7 @@ sys.path.insert(0, ROOT)
 METRIC = "H' build GB/s (bytes read+written)"
 L2_BYTES = 126 << 20
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
-REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+REF_DIR = os.environ.get("LFBP_REF_DIR") or os.path.join(ROOT, "baseline", "_ref")  # the reference install
 
 
 def _peaks():
@@ -202,39 +204,121 @@ def _port_planes(w, requested: int) -> int:
     return max(1, min(w.shape[4], (3 << 29) // (w.plane_elems * w.itemsize)))
 
 
+def _ref_plane_worker(wname, z, steps, warmup, bar, q):
+    """One process of the reference arm: the unmodified lfbp (baseline/_ref)
+    transforms plane z of the workload `warmup` + `steps` times; the timed
+    steps start together (barrier) and report (t_start, t_end, digest)."""
+    try:
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        import lfbp  # noqa: E402  (the reference package, unmodified)
+
+        from paper_2003_09133_b200.configs import WORKLOADS
+        from paper_2003_09133_b200.synth import baseline_psf
+        w = WORKLOADS[wname]
+        H = baseline_psf(w, z, z + 1, threads=1)
+        psf = lfbp.PsfArray._wrap(lfbp.Dims5(*H.shape), H)
+        for _ in range(warmup):
+            lfbp.compute_backprojection(psf)
+        spans, digest = [], None
+        for _ in range(steps):
+            bar.wait()
+            t0 = time.time()
+            bp = lfbp.compute_backprojection(psf)
+            spans.append((t0, time.time()))
+            digest = hashlib.sha256(bp.data.tobytes(order="F")).hexdigest()
+            del bp
+        q.put((z, spans, digest, H.nbytes, None))
+    except BaseException as e:  # report, never hang the barrier of the others
+        bar.abort()
+        q.put((z, None, None, 0, f"{type(e).__name__}: {e}"))
+
+
+def run_reference_processes(args, w, procs: int):
+    """The unmodified reference on `procs` planes at once, one process per
+    plane (planes are independent, reference test_transform.py:141-154);
+    step time = last end - first start over the processes."""
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    nz = w.shape[4]
+    zs = [(nz // 2 - procs // 2 + k) % nz for k in range(procs)]
+    bar = ctx.Barrier(procs)
+    q = ctx.Queue()
+    warm = min(args.warmup, 1)
+    ps = [ctx.Process(target=_ref_plane_worker, args=(w.name, z, args.steps, warm, bar, q)) for z in zs]
+    for pr in ps:
+        pr.start()
+    res = [q.get() for _ in ps]
+    for pr in ps:
+        pr.join()
+    errs = [r[4] for r in res if r[4]]
+    if errs:
+        raise RuntimeError(errs[0])
+    step_s = [max(r[1][k][1] for r in res) - min(r[1][k][0] for r in res) for k in range(args.steps)]
+    want = _golden_plane_digests(w)
+    ok = None if want is None else all(r[2] == want[r[0]] for r in res)
+    nbytes = sum(2 * r[3] for r in res)
+    return step_s, nbytes, sorted(zs), ok, warm
+
+
 def run_reference(args, w):
-    """--impl reference: the CPU arm (the oracle port, every host thread) on a
-    bounded plane sample of the same workload, per step."""
+    """--impl reference: the reference's own CPU path on the box's host cores.
+    With baseline/_ref installed this is the UNMODIFIED lfbp.compute_backprojection
+    (single-threaded numpy as shipped), one process per plane on every host
+    thread; without it, the oracle's numpy restatement on every host thread.
+    Each step is a bounded plane sample of the same workload."""
     rank, world, _ = _dist()
     if world > 1 and rank != 0:
         return 0
-    from oracle.hprime_oracle import hprime_oracle_split
-    from paper_2003_09133_b200.synth import baseline_psf
-    planes = _port_planes(w, args.cpu_planes)
     threads = _threads()
-    z0 = max(0, w.shape[4] // 2 - planes // 2)
-    H = baseline_psf(w, z0, z0 + planes)
-    for _ in range(args.warmup):
-        hprime_oracle_split(H, threads)
-    times = []
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        hprime_oracle_split(H, threads)
-        times.append(time.perf_counter() - t)
+    sample = None
+    if os.path.isdir(os.path.join(REF_DIR, "lfbp")):
+        procs = max(1, min(threads, w.shape[4], args.cpu_planes or threads))
+        # bound host memory: ~3 x plane bytes per process (reference peak RSS)
+        try:
+            avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+            procs = max(1, min(procs, int(0.6 * avail // (4 * w.plane_elems * w.itemsize))))
+        except (ValueError, OSError):
+            pass
+        times, nbytes, zs, ok, warm = run_reference_processes(args, w, procs)
+        kind, cores = "reference", procs
+        what = ("lfbp.compute_backprojection from baseline/_ref (the unmodified reference, single-threaded "
+                "numpy as shipped), one process per plane")
+        sample = (f"{procs} planes {zs[0]}..{zs[-1]} of {w.shape[4]} of {w.name} per step, one per process "
+                  f"(chunked: planes are independent, reference test_transform.py:141-154); warm-up {warm}")
+        extra = {"matches_reference_digests": ok}
+    else:
+        from oracle.hprime_oracle import hprime_oracle_split
+        from paper_2003_09133_b200.synth import baseline_psf
+        planes = _port_planes(w, args.cpu_planes)
+        z0 = max(0, w.shape[4] // 2 - planes // 2)
+        H = baseline_psf(w, z0, z0 + planes)
+        for _ in range(args.warmup):
+            hprime_oracle_split(H, threads)
+        times = []
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            hprime_oracle_split(H, threads)
+            times.append(time.perf_counter() - t)
+        nbytes = 2 * H.nbytes
+        kind, cores = "port", threads
+        what = ("oracle/hprime_oracle.py: numpy restatement of lfbp.compute_backprojection "
+                "(transform.py:113-135), planes and output columns split over host threads "
+                "(baseline/_ref not installed)")
+        sample = (f"planes [{z0}, {z0 + planes}) of {w.shape[4]} of {w.name} per step (chunked: planes are "
+                  f"independent, reference test_transform.py:141-154)")
+        extra = {}
     total = sum(times)
-    gbs = 2 * H.nbytes * args.steps / total / 1e9
-    sample = (f"planes [{z0}, {z0 + planes}) of {w.shape[4]} of {w.name} per step (chunked: planes are "
-              f"independent, reference test_transform.py:141-154)")
+    gbs = nbytes * args.steps / total / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
         "higher_is_better": True, "scaling": "strong" if not args.weak else "weak", "vs_baseline": None,
         "dtype": _dtype_tag(w.dtype), "data": "synthetic (seeded BASELINE.json law, see synth.py)",
-        "config": {"workload": _workload_tag(w), "sample_planes": planes},
-        "helems_per_s": round(H.size * args.steps / total, 1),
-        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample,
-                         "what": "oracle/hprime_oracle.py: numpy restatement of lfbp.compute_backprojection "
-                                 "(transform.py:113-135), planes and output columns split over host threads"},
+        "config": {"workload": _workload_tag(w)},
+        "helems_per_s": round(nbytes / (2 * w.itemsize) * args.steps / total, 1),
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+                         "what": what, "host_threads_available": threads, **extra},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

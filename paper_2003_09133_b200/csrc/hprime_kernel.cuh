@@ -182,7 +182,10 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 // + 32 producers, ...), completion on `bar` (one expect_tx arrive per
 // producer warp).  The bulk copies take uniform operands, so ptxas issues a
 // warp's runs one lane at a time; several producer warps issue in parallel.
-template <int E>
+// TASKS: run x's aligned superset starts at stage + 80 + x * row_pitch (row
+// pitch a multiple of 16), so element k of run x sits at that address plus
+// (run byte offset mod 16) + k * E; the task consumer resolves x per task.
+template <int E, bool TASKS>
 __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __restrict__ src, uint32_t u,
                                            uint8_t* stage, uint32_t bar, int lane, int pw, uint64_t policy) {
   using T = typename Word<E>::T;
@@ -203,7 +206,8 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
       if (a_hi > lim) a_hi = lim > a_lo ? lim : a_lo;
       // element k of run x lives at R0 + x*row_pitch + k*E (see hprime_plan.h);
       // its 16-byte aligned superset starts (b & 15) bytes earlier
-      uint8_t* dst = stage + kHdrBytes + 16 + (b0 & 15) + static_cast<int64_t>(x) * p.row_pitch - (b & 15);
+      uint8_t* dst = TASKS ? stage + kHdrBytes + 16 + static_cast<int64_t>(x) * p.row_pitch
+                           : stage + kHdrBytes + 16 + (b0 & 15) + static_cast<int64_t>(x) * p.row_pitch - (b & 15);
 #if defined(HP_DBG_NOLOAD)  // pattern probe build: no reads of H
       a_hi = a_lo;
 #endif
@@ -469,9 +473,145 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
   }
 }
 
+__device__ __forceinline__ int32_t atom_add_smem(int* p, int32_t v) {
+  int32_t old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
+}
+
+// HP_FLAG_TASKS consumer.  A task is (output row r, phase class c < n_x):
+// the 16-byte groups g = c, c + n_x, c + 2 n_x, ... of row r.  Stepping n_x
+// groups moves VE * n_x elements along i, which brings the source phase
+// x = (x' + i - c_s) mod n_x back to the same value for every element of the
+// group, so the VE shared-memory addresses of a task's groups are VE fixed
+// bases minus m * 16 n_x bytes: the steady loop is VE LDS, VE address adds
+// and one 16-byte store per group, with no wrap selects.  All per-row and
+// per-phase index arithmetic (the mirror, the phase and the row's 16-byte
+// alignment) happens once per task.  Lanes take consecutive tasks (32 per
+// claim), so the classes of one row go to neighbouring lanes and a warp's
+// stores cover ~16 n_x contiguous bytes of a row.
+template <int E>
+__device__ __forceinline__ void consume_unit_tasks(const HpPlan& p, uint8_t* __restrict__ dst, const uint8_t* stage,
+                                                   uint32_t stage_s, int lane) {
+  using T = typename Word<E>::T;
+  constexpr int VE = 16 / E;
+  const UnitHdr h = *reinterpret_cast<const UnitHdr*>(stage);
+  const int32_t n_x = static_cast<int32_t>(p.n_x);
+  const int32_t n_s = static_cast<int32_t>(p.n_s);
+  const int32_t n_t = static_cast<int32_t>(p.n_t);
+  const int32_t xs = n_s * n_t;                       // in-plane offsets are 32-bit
+  const int32_t ntask = h.jb * n_x * n_x;
+  const int32_t i_lo = h.i_lo, i_hi = h.i_hi;
+  const int32_t i_end = min(i_hi, p.v_s);              // loaded elements: [i_lo, i_end)
+  const int32_t zmis = static_cast<int32_t>(h.plane_off & (VE - 1));
+  const int32_t rp = p.row_pitch;
+  const int32_t dstep = 16 * n_x;                      // smem bytes per n_x groups
+  const int32_t ostep = VE * n_x;                      // H' elements per n_x groups
+  const uint32_t sbase = stage_s + kHdrBytes + 16;
+  const int32_t kbase = 2 * p.c_s - h.s_lo;            // k = tl * n_s + kbase - i
+  T* dz = reinterpret_cast<T*>(dst) + h.plane_off;
+  int* counter = &reinterpret_cast<UnitHdr*>(const_cast<uint8_t*>(stage))->next_row;
+  int32_t claim = 0;
+  if (lane == 0) claim = atom_add_smem(counter, 32);
+  for (;;) {
+    const int32_t tb = __shfl_sync(0xffffffffu, claim, 0);
+    if (tb >= ntask) break;
+    if (lane == 0) claim = atom_add_smem(counter, 32);
+    const int32_t task = tb + lane;
+    if (task >= ntask) continue;
+    const int32_t r = static_cast<int32_t>(hp_div(p.nx_div, static_cast<uint32_t>(task)));
+    const int32_t c = task - r * n_x;
+    const int32_t tl = static_cast<int32_t>(hp_div(p.nx_div, static_cast<uint32_t>(r)));
+    const int32_t xp = r - tl * n_x;
+    const int32_t t = h.t0 + tl;
+    const bool zero_row = t >= p.v_t;  // dropped source row t = n_t - 1 (even n_t)
+    const int32_t j = zero_row ? n_t - 1 : 2 * p.c_t - t;
+    const int32_t yp = zero_row ? h.y : static_cast<int32_t>(hp_mod(p.ny_div, static_cast<uint32_t>(h.y + t + p.ny_off)));
+    const int32_t o_in = n_s * j + xs * (xp + n_x * yp);
+    T* orow = dz + o_in;
+    if (c == 0 && i_end < i_hi) orow[n_s - 1] = T(0);  // even n_s: row i = n_s - 1 is zero
+    const int32_t gs = i_lo - ((o_in + zmis + i_lo) & (VE - 1));   // first group start (element i)
+    const int32_t ng = i_end > i_lo ? (i_end - gs + VE - 1) / VE : 0;
+    if (c >= ng) continue;
+    const int32_t cnt = static_cast<int32_t>(hp_div(p.nx_div, static_cast<uint32_t>(ng - c - 1))) + 1;
+    const int32_t i0 = gs + VE * c;                    // first element of the task's group m = 0
+    T* o = orow + i0;
+    const bool head = c == 0 && gs < i_lo;             // group 0 starts before i_lo
+    const bool tail = c + (cnt - 1) * n_x == ng - 1 && ((i_end - gs) & (VE - 1)) != 0;
+    if (zero_row) {
+      for (int32_t m = 0; m < cnt; ++m)
+#pragma unroll
+        for (int q = 0; q < VE; ++q) {
+          const int32_t i = i0 + m * ostep + q;
+          if (i >= i_lo && i < i_end) o[m * ostep + q] = T(0);
+        }
+      continue;
+    }
+    // smem address of element q of group m: A[q] - m * dstep
+    uint32_t A[VE];
+    const uint32_t x0 = static_cast<uint32_t>(xp + i0 + p.nx_off + VE * n_x);  // >= 0
+    const int32_t k0 = tl * n_s + kbase - i0;
+#pragma unroll
+    for (int q = 0; q < VE; ++q) {
+      const uint32_t x = hp_mod(p.nx_div, x0 + q);
+      A[q] = sbase + x * rp + ((h.o0 + x * p.xs16) & 15) + static_cast<uint32_t>((k0 - q) * E);
+    }
+    auto masked = [&](int32_t m) {
+      const uint32_t off = static_cast<uint32_t>(m * dstep);
+#pragma unroll
+      for (int q = 0; q < VE; ++q) {
+        const int32_t i = i0 + m * ostep + q;
+        if (i >= i_lo && i < i_end) o[m * ostep + q] = lds<E>(A[q] - off);
+      }
+    };
+    const int32_t m0 = head ? 1 : 0;
+    const int32_t m1 = tail ? cnt - 1 : cnt;
+    if (head) masked(0);
+    if (m0 < m1) {  // full groups, software-pipelined, two alternating register sets
+      T va[VE], vb[VE];
+      uint32_t a = A[0] - static_cast<uint32_t>(m0 * dstep);
+      const uint32_t d1 = A[1] - A[0], d2 = A[VE > 2 ? 2 : 1] - A[0], d3 = A[VE - 1] - A[0];
+      auto load = [&](T* v) {
+        v[0] = lds<E>(a);
+        if constexpr (VE == 2) {
+          v[1] = lds<E>(a + d1);
+        } else {
+          v[1] = lds<E>(a + d1);
+          v[2] = lds<E>(a + d2);
+          v[3] = lds<E>(a + d3);
+        }
+      };
+      T* oo = o + m0 * ostep;
+      int32_t m = m0;
+      load(va);
+      for (;;) {
+        if (++m >= m1) {
+          st_vec<E>(oo, va);
+          break;
+        }
+        a -= dstep;
+        T* oa = oo;
+        oo += ostep;
+        load(vb);
+        st_vec<E>(oa, va);
+        if (++m >= m1) {
+          st_vec<E>(oo, vb);
+          break;
+        }
+        a -= dstep;
+        T* ob = oo;
+        oo += ostep;
+        load(va);
+        st_vec<E>(ob, vb);
+      }
+    }
+    if (tail && !(head && cnt == 1)) masked(cnt - 1);
+  }
+}
+
 // Warps 0..producers-1 produce, the rest consume; full/empty mbarrier ring
 // of `stages` buffers, so consumer warps never wait for each other.
-template <int E>
+template <int E, bool TASKS>
 __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const uint8_t* __restrict__ src,
                                                      uint8_t* __restrict__ dst) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -503,8 +643,8 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
         mbar_wait(smem_u32(&empty[st]), ph ^ 1u);
         fence_proxy_async_smem();
       }
-      issue_unit<E>(p, src, first + k * stride, stages + static_cast<int64_t>(st) * p.stage_bytes,
-                    smem_u32(&full[st]), lane, warp, policy);
+      issue_unit<E, TASKS>(p, src, first + k * stride, stages + static_cast<int64_t>(st) * p.stage_bytes,
+                           smem_u32(&full[st]), lane, warp, policy);
       if (++st == S) {
         st = 0;
         ph ^= 1u;
@@ -517,8 +657,12 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
   uint32_t ph = 0;
   for (uint32_t k = 0; k < mine; ++k) {
     mbar_wait(smem_u32(&full[st]), ph);
-    consume_unit<E>(p, dst, stages + static_cast<int64_t>(st) * p.stage_bytes,
-                    stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - np, nc, lane);
+    if constexpr (TASKS)
+      consume_unit_tasks<E>(p, dst, stages + static_cast<int64_t>(st) * p.stage_bytes,
+                            stage0 + static_cast<uint32_t>(st) * p.stage_bytes, lane);
+    else
+      consume_unit<E>(p, dst, stages + static_cast<int64_t>(st) * p.stage_bytes,
+                      stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - np, nc, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     if (++st == S) {

@@ -67,6 +67,8 @@ HP_HD uint32_t hp_mod(const HpFastDiv& f, uint32_t n) {
 #define HP_FLAG_BAND_FASTEST 4      // unit order: t-band fastest instead of y
 #define HP_FLAG_DIAGONAL 8          // unit order: t-band fastest along a y' = y + t - c_t diagonal
 #define HP_FLAG_ROTATE 16           // unit u issues its runs / claims its rows starting at u mod n
+#define HP_FLAG_TASKS 32            // (row, phase-class) task consumer and 16-byte row pitch (see
+                                    // consume_unit_tasks in hprime_kernel.cuh)
 
 struct HpPlan {
   // geometry of the (chunk) arrays the kernel sees
@@ -82,7 +84,8 @@ struct HpPlan {
   int32_t n_bands;            // ceil(n_t / J)
   int32_t C;                  // output i per unit (chunk); == n_s when unchunked
   int32_t n_chunks;           // ceil(n_s / C)
-  int32_t row_pitch;          // smem bytes between staged runs (== xs16 mod 16)
+  int32_t row_pitch;          // smem bytes between staged runs (== xs16 mod 16; a multiple
+                              // of 16 with HP_FLAG_TASKS)
   int32_t stage_bytes;        // n_x * row_pitch + 32 rounded to 128
   int32_t stages;             // smem ring depth
   int32_t threads;            // CTA size: 1 producer warp + consumer warps

@@ -87,8 +87,10 @@ DevProps device_props(int dev) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(dev);
-    cudaFuncSetAttribute(hp::hprime_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
-    cudaFuncSetAttribute(hp::hprime_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
+    cudaFuncSetAttribute(hp::hprime_kernel<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
+    cudaFuncSetAttribute(hp::hprime_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
+    cudaFuncSetAttribute(hp::hprime_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
+    cudaFuncSetAttribute(hp::hprime_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
     cudaSetDevice(cur);
   } else {
     cudaGetLastError();  // clear "no device" state
@@ -164,6 +166,49 @@ constexpr int kNumCandidates = int(sizeof(kCandidates) / sizeof(kCandidates[0]))
 constexpr int kNumSmallCandidates = int(sizeof(kSmallCandidates) / sizeof(kSmallCandidates[0]));
 static_assert(kNumSmallCandidates <= kNumCandidates, "arrays in autotune() are sized by the large set");
 
+// Average shared-memory wavefronts per LDS of the task consumer
+// (consume_unit_tasks) on the first unit of plane 0 with row pitch `rp`:
+// the 32 lanes of a warp take consecutive (row, phase class) tasks.  Used
+// to pick the pitch; a model, not a measurement.
+double task_bank_cost(const int64_t d[5], int E, int J, int C, int32_t rp) {
+  const int64_t n_s = d[0], n_t = d[1], n_x = d[2], n_y = d[3];
+  const int VE = 16 / E;
+  const int64_t c_s = (n_s - 1) / 2, c_t = (n_t - 1) / 2;
+  const int64_t nx_off = (n_x - (c_s % n_x)) % n_x, ny_off = (n_y - (c_t % n_y)) % n_y;
+  const int64_t xs16 = (n_s * n_t * E) & 15;
+  const int64_t ntask = std::min<int64_t>(int64_t(J) * n_x * n_x, 32 * 16);
+  const int64_t i_end = std::min<int64_t>(C, 2 * c_s + 1);
+  double waves = 0;
+  int n = 0;
+  for (int64_t t0 = 0; t0 < ntask; t0 += 32) {
+    for (int q = 0; q < VE; ++q) {
+      int64_t words[32 * 2];
+      int nw = 0;
+      for (int64_t task = t0; task < std::min<int64_t>(t0 + 32, ntask); ++task) {
+        const int64_t r = task / n_x, c = task % n_x, tl = r / n_x, xp = r % n_x;
+        if (tl >= n_t) continue;
+        const int64_t j = 2 * c_t - tl, yp = (tl + ny_off) % n_y;
+        const int64_t o_in = n_s * j + n_s * n_t * (xp + n_x * yp);
+        const int64_t gs = -(o_in & (VE - 1));
+        const int64_t i = gs + VE * c + q;
+        if (i < 0 || i >= i_end) continue;
+        const int64_t x = (xp + i + nx_off) % n_x;
+        const int64_t k = tl * n_s + 2 * c_s - i;
+        const int64_t a = 80 + x * rp + ((x * xs16) & 15) + k * E;
+        for (int h = 0; h < E / 4; ++h) words[nw++] = a / 4 + h;
+      }
+      std::sort(words, words + nw);
+      const int nu = int(std::unique(words, words + nw) - words);
+      int per_bank[32] = {0};
+      int worst = 0;
+      for (int u = 0; u < nu; ++u) worst = std::max(worst, ++per_bank[words[u] & 31]);
+      waves += worst;
+      ++n;
+    }
+  }
+  return n ? waves / n : 0.0;
+}
+
 // Work-unit shape, smem ring and persistent grid for one launch.
 int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_count,
               int64_t total_bytes, int dev, const Knobs& kn = Knobs()) {
@@ -214,10 +259,33 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   p.n_bands = static_cast<int32_t>((d[1] + p.J - 1) / p.J);
   // row pitch: >= run + 32 B, congruent to xs16 mod 16 (linear x addressing,
   // see hprime_plan.h); the multiple-of-16 part is odd to spread banks
+  p.flags = env_int("LFBP_KFLAGS", kn.flags);
+  const bool tasks = (p.flags & HP_FLAG_TASKS) != 0;
   int64_t pitch = round_up(run_max + 32, 16);
-  if (((pitch / 16) & 1) == 0) pitch += 16;
-  pitch += env_int("LFBP_PITCH_EXTRA16", 0) * 16;
-  p.row_pitch = static_cast<int32_t>(pitch + p.xs16);
+  if (tasks) {
+    // task consumer: any multiple of 16; pick the one with the fewest
+    // shared-memory wavefronts for a warp's 32 tasks (task_bank_cost)
+    const int extra = env_int("LFBP_PITCH_EXTRA16", -1);
+    if (extra >= 0) {
+      pitch += 16 * extra;
+    } else {
+      int64_t best = pitch;
+      double best_cost = 1e30;
+      for (int e = 0; e < 8; ++e) {
+        const double c = task_bank_cost(d, E, p.J, p.C, static_cast<int32_t>(pitch + 16 * e));
+        if (c < best_cost - 1e-9) {
+          best_cost = c;
+          best = pitch + 16 * e;
+        }
+      }
+      pitch = best;
+    }
+    p.row_pitch = static_cast<int32_t>(pitch);
+  } else {
+    if (((pitch / 16) & 1) == 0) pitch += 16;
+    pitch += env_int("LFBP_PITCH_EXTRA16", 0) * 16;
+    p.row_pitch = static_cast<int32_t>(pitch + p.xs16);
+  }
   p.stage_bytes = static_cast<int32_t>(round_up(64 + d[2] * p.row_pitch + 32, 128));  // header + runs
   int S = env_int("LFBP_STAGES", kn.stages);
   S = std::max(1, std::min(S, 8));
@@ -242,10 +310,11 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   p.n_units = units;
   int per_sm = 0;
   if (dp.real) {
-    cudaError_t e = (E == 4) ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hp::hprime_kernel<4>,
-                                                                           threads, p.smem_bytes)
-                             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hp::hprime_kernel<8>,
-                                                                           threads, p.smem_bytes);
+    const void* fn = (E == 4) ? (tasks ? reinterpret_cast<const void*>(hp::hprime_kernel<4, true>)
+                                       : reinterpret_cast<const void*>(hp::hprime_kernel<4, false>))
+                              : (tasks ? reinterpret_cast<const void*>(hp::hprime_kernel<8, true>)
+                                       : reinterpret_cast<const void*>(hp::hprime_kernel<8, false>));
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, p.smem_bytes);
     if (e != cudaSuccess) return fail(LFBP_ERR_CUDA, "occupancy query: %s", cudaGetErrorString(e));
   } else {
     per_sm = std::min<int>(dp.max_threads_sm / threads, int((233472) / (p.smem_bytes + 1024)));
@@ -257,7 +326,6 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   p.grid = static_cast<int32_t>(std::min<int64_t>(units, int64_t(per_sm) * dp.sm_count));
   const int grid_cap = env_int("LFBP_GRID", kn.grid_sm);  // fewer persistent CTAs
   if (grid_cap > 0) p.grid = std::min<int32_t>(p.grid, int32_t(int64_t(grid_cap) * per_sm));
-  p.flags = env_int("LFBP_KFLAGS", kn.flags);
   // lanes per output row: enough 16-byte groups per lane to amortise the row setup
   const int64_t groups = (std::min<int64_t>(p.C, d[0]) * E + 15) / 16 + 1;
   int W = env_int("LFBP_SUBWARP", kn.subwarp);
@@ -287,12 +355,20 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
 
 int launch(const HpPlan& p, const void* src, void* dst, cudaStream_t st) {
   if (p.n_units == 0) return LFBP_OK;
-  if (p.elem == 4)
-    hp::hprime_kernel<4><<<p.grid, p.threads, p.smem_bytes, st>>>(p, static_cast<const uint8_t*>(src),
-                                                                   static_cast<uint8_t*>(dst));
-  else
-    hp::hprime_kernel<8><<<p.grid, p.threads, p.smem_bytes, st>>>(p, static_cast<const uint8_t*>(src),
-                                                                   static_cast<uint8_t*>(dst));
+  const uint8_t* s8 = static_cast<const uint8_t*>(src);
+  uint8_t* d8 = static_cast<uint8_t*>(dst);
+  const bool tasks = (p.flags & HP_FLAG_TASKS) != 0;
+  if (p.elem == 4) {
+    if (tasks)
+      hp::hprime_kernel<4, true><<<p.grid, p.threads, p.smem_bytes, st>>>(p, s8, d8);
+    else
+      hp::hprime_kernel<4, false><<<p.grid, p.threads, p.smem_bytes, st>>>(p, s8, d8);
+  } else {
+    if (tasks)
+      hp::hprime_kernel<8, true><<<p.grid, p.threads, p.smem_bytes, st>>>(p, s8, d8);
+    else
+      hp::hprime_kernel<8, false><<<p.grid, p.threads, p.smem_bytes, st>>>(p, s8, d8);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   HP_CUDA(cudaGetLastError());
   return LFBP_OK;

@@ -8,10 +8,24 @@ import sys
 from conftest import ROOT
 
 
-def test_reference_arm_json_line():
+import pytest
+
+REF_INSTALLED = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "lfbp"))
+
+
+@pytest.mark.parametrize("arm", ["reference", "port"])
+def test_reference_arm_json_line(arm):
+    """The reference arm: the unmodified lfbp from baseline/_ref, one process
+    per plane (kind "reference", checked against the reference's digests),
+    or the oracle port when the reference is not installed."""
+    if arm == "reference" and not REF_INSTALLED:
+        pytest.skip("baseline/_ref not installed (tools/install_reference.sh)")
+    env = dict(os.environ)
+    if arm == "port":
+        env["LFBP_REF_DIR"] = os.path.join(ROOT, "no-such-dir")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
                         "--steps", "2", "--warmup", "1", "--cpu-planes", "2"],
-                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -20,7 +34,9 @@ def test_reference_arm_json_line():
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in d, key
     assert d["impl"] == "reference" and d["unit"] == "GB/s" and d["value"] > 0
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] == arm and d["cpu_baseline"]["cores"] >= 1
+    if arm == "reference":
+        assert d["cpu_baseline"]["matches_reference_digests"] is True
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["dtype"] == "f32"
 
 
