@@ -154,6 +154,9 @@ const Knobs kCandidates[] = {
     // plan oversubscribes the memory system on some boxes (profiles/r02_*)
     {3, 64, 8, 32, HP_FLAG_DIAGONAL}, {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ROTATE},
     {3, 64, 8, 32, HP_FLAG_DIAGONAL, 140}, {3, 64, 8, 32, 0, 140}, {3, 64, 8, 32, HP_FLAG_ROTATE},
+    // the (row, phase-class) task consumer: C3 +3-5 %, C2 J = 8 on par
+    // (profiles/r02_tasks_ab.jsonl)
+    {4, 48, 12, 0, HP_FLAG_TASKS}, {2, 96, 12, 0, HP_FLAG_TASKS},
 };
 // Small problems (8-256 MB moved) are latency-bound: smaller stages (narrower
 // t-bands, several CTAs per SM) and short-row sub-warps; measured on the
