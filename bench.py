@@ -574,14 +574,20 @@ def main():
         peak, peak_src = _peaks()
         avg_kern_ms = statistics.mean(kern_ms)
         achieved = step_bytes / (avg_kern_ms * 1e-3) / 1e9
-        traffic = None
+        traffic = traffic_src = None
         prof = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
         if os.path.exists(prof):
             try:
                 with open(prof) as f:
                     pj = json.load(f)
-                if pj.get("workload") == w.name and pj.get("shape") == list(shape):
-                    traffic = pj.get("dram_bytes_per_launch")
+                # a capture of the same plane geometry (a z-slab of the workload
+                # for C5, whose 142 GB ncu would have to save and restore per
+                # replay pass) scales by planes: K1's traffic is per plane
+                ps = pj.get("shape")
+                if pj.get("workload") == w.name and ps and list(ps[:4]) == list(shape[:4]) and ps[4] > 0:
+                    traffic = round(pj["dram_bytes_per_launch"] * shape[4] / ps[4])
+                    traffic_src = f"{pj.get('source')} ({ps[4]}-plane capture, scaled to {shape[4]} planes)" \
+                        if ps[4] != shape[4] else pj.get("source")
             except (OSError, ValueError):
                 pass
         total_bytes = (world if args.weak else 1) * (step_bytes if args.weak else 2 * w.nbytes)
@@ -606,7 +612,8 @@ def main():
             "helems_per_s": round(total_bytes / (2 * w.itemsize) * args.steps / (max_ms * 1e-3), 1),
             "frac_of_8tbs_nominal": round(value / world / 8000.0, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "kernel": "hp::hprime_kernel (K1)", "kernel_ms_avg": round(avg_kern_ms, 4),
                          "kernel_ms_min": round(min(kern_ms), 4),
                          "algorithmic_bytes_per_launch": step_bytes},

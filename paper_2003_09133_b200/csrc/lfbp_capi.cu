@@ -154,6 +154,12 @@ const Knobs kCandidates[] = {
     // plan oversubscribes the memory system on some boxes (profiles/r02_*)
     {3, 64, 8, 32, HP_FLAG_DIAGONAL}, {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ROTATE},
     {3, 64, 8, 32, HP_FLAG_DIAGONAL, 140}, {3, 64, 8, 32, 0, 140}, {3, 64, 8, 32, HP_FLAG_ROTATE},
+    // C5 demand exceeds the DRAM supply with all 148 SMs and the rate collapses
+    // (5.94 TB/s); per SM it holds 44.8 GB/s up to 145 SMs: 6.45 TB/s there
+    // (profiles/r02_grid_sweep_fine.jsonl).  The cliff sits at a box-dependent
+    // SM count, so the tuner times both sides of it.
+    {3, 64, 8, 32, HP_FLAG_DIAGONAL, 144}, {3, 64, 8, 32, HP_FLAG_DIAGONAL, 145},
+    {4, 64, 8, 32, HP_FLAG_DIAGONAL, 146},
     // the (row, phase-class) task consumer: C3 +3-5 %, C2 J = 8 on par
     // (profiles/r02_tasks_ab.jsonl)
     {4, 48, 12, 0, HP_FLAG_TASKS}, {2, 96, 12, 0, HP_FLAG_TASKS},
