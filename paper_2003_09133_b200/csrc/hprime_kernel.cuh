@@ -85,6 +85,7 @@ struct UnitHdr {
   int32_t y, t0, jb, i_lo, i_hi, s_lo, o0;
   int32_t next_row;     // work counter: consumer warps claim rows with atomicAdd
   int32_t rot;          // HP_FLAG_ROTATE: rows are claimed starting at this one
+  int32_t stop;         // HP_FLAG_DYNAMIC: no unit in this stage, the consumers exit
 };
 constexpr int kHdrBytes = 64;
 
@@ -236,6 +237,7 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
     h->o0 = static_cast<int32_t>(b0 & 15);
     h->next_row = 0;
     h->rot = (p.flags & HP_FLAG_ROTATE) ? static_cast<int32_t>(u % static_cast<uint32_t>(w.jb * p.n_x)) : 0;
+    h->stop = 0;
   }
   tx = __reduce_add_sync(0xffffffffu, tx);
   __syncwarp();                                    // header and tail stores before the release
@@ -634,10 +636,43 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
     fence_barrier_init();
   }
   __syncthreads();
+  const bool dynamic = (p.flags & HP_FLAG_DYNAMIC) != 0;  // planner: only with one producer warp
   if (warp < np) {
     const uint64_t policy = policy_evict_first();
     int st = 0;
     uint32_t ph = 0;
+    if (dynamic) {
+      // units are handed out in global order by one counter per launch, so
+      // the units in flight always form one window of ~grid * stages units
+      // and no CTA drifts ahead of the others; the next ticket is fetched
+      // while the current unit is issued
+      unsigned long long* ctr = p.counter;
+      uint32_t u = 0, nxt = 0;
+      if (lane == 0) u = static_cast<uint32_t>(atomicAdd(ctr, 1ull));
+      u = __shfl_sync(0xffffffffu, u, 0);
+      for (uint32_t k = 0;; ++k) {
+        if (k >= static_cast<uint32_t>(S)) {
+          mbar_wait(smem_u32(&empty[st]), ph ^ 1u);
+          fence_proxy_async_smem();
+        }
+        uint8_t* stage = stages + static_cast<int64_t>(st) * p.stage_bytes;
+        if (u >= n_units) {
+          if (lane == 0) {
+            reinterpret_cast<UnitHdr*>(stage)->stop = 1;
+            mbar_arrive_expect_tx(smem_u32(&full[st]), 0);
+          }
+          break;
+        }
+        if (lane == 0) nxt = static_cast<uint32_t>(atomicAdd(ctr, 1ull));
+        issue_unit<E, TASKS>(p, src, u, stage, smem_u32(&full[st]), lane, warp, policy);
+        u = __shfl_sync(0xffffffffu, nxt, 0);
+        if (++st == S) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+      return;
+    }
     for (uint32_t k = 0; k < mine; ++k) {
       if (k >= static_cast<uint32_t>(S)) {
         mbar_wait(smem_u32(&empty[st]), ph ^ 1u);
@@ -655,14 +690,14 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
   const uint32_t stage0 = smem_u32(stages);
   int st = 0;
   uint32_t ph = 0;
-  for (uint32_t k = 0; k < mine; ++k) {
+  for (uint32_t k = 0; dynamic || k < mine; ++k) {
     mbar_wait(smem_u32(&full[st]), ph);
+    const uint8_t* stage = stages + static_cast<int64_t>(st) * p.stage_bytes;
+    if (dynamic && reinterpret_cast<const volatile UnitHdr*>(stage)->stop) break;
     if constexpr (TASKS)
-      consume_unit_tasks<E>(p, dst, stages + static_cast<int64_t>(st) * p.stage_bytes,
-                            stage0 + static_cast<uint32_t>(st) * p.stage_bytes, lane);
+      consume_unit_tasks<E>(p, dst, stage, stage0 + static_cast<uint32_t>(st) * p.stage_bytes, lane);
     else
-      consume_unit<E>(p, dst, stages + static_cast<int64_t>(st) * p.stage_bytes,
-                      stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - np, nc, lane);
+      consume_unit<E>(p, dst, stage, stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - np, nc, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     if (++st == S) {

@@ -69,6 +69,8 @@ HP_HD uint32_t hp_mod(const HpFastDiv& f, uint32_t n) {
 #define HP_FLAG_ROTATE 16           // unit u issues its runs / claims its rows starting at u mod n
 #define HP_FLAG_TASKS 32            // (row, phase-class) task consumer and 16-byte row pitch (see
                                     // consume_unit_tasks in hprime_kernel.cuh)
+#define HP_FLAG_ZCHUNK 64           // host side: one launch per ~12 GB z-slab (launch() in lfbp_capi.cu)
+#define HP_FLAG_DYNAMIC 128         // units handed out in order by a per-launch global counter
 
 struct HpPlan {
   // geometry of the (chunk) arrays the kernel sees
@@ -109,6 +111,7 @@ struct HpPlan {
   HpFastDiv zc_div;           // n_y * n_bands: units per (z, chunk)
   HpFastDiv yblk_div;         // tile_y * n_bands: units per full y block
   HpFastDiv ty_div, tyl_div;  // tile_y, and the last block's y count
+  unsigned long long* counter;  // HP_FLAG_DYNAMIC: zeroed unit ticket counter (set per launch)
 };
 
 // Valid Dims5 (reference arrays.py:53-67): all >= 1, n_x and n_y odd,

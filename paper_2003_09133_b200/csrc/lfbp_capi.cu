@@ -160,6 +160,10 @@ const Knobs kCandidates[] = {
     // SM count, so the tuner times both sides of it.
     {3, 64, 8, 32, HP_FLAG_DIAGONAL, 144}, {3, 64, 8, 32, HP_FLAG_DIAGONAL, 145},
     {4, 64, 8, 32, HP_FLAG_DIAGONAL, 146},
+    // ... and with ~12 GB launches (HP_FLAG_ZCHUNK) the full grid holds
+    // 6.35 TB/s on the whole C5 array (profiles/r02_zchunk.jsonl)
+    {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ZCHUNK}, {3, 64, 8, 32, HP_FLAG_ZCHUNK},
+    {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ZCHUNK, 145},
     // the (row, phase-class) task consumer: C3 +3-5 %, C2 J = 8 on par
     // (profiles/r02_tasks_ab.jsonl)
     {4, 48, 12, 0, HP_FLAG_TASKS}, {2, 96, 12, 0, HP_FLAG_TASKS},
@@ -311,6 +315,7 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   int prod = env_int("LFBP_PRODUCERS", int((d[2] + 31) / 32));
   prod = std::max(1, std::min(prod, 17 - cwarps));
   p.producers = prod;
+  if (prod > 1) p.flags &= ~HP_FLAG_DYNAMIC;  // the ticket is taken by the one producer warp
   const int threads = 32 * (prod + cwarps);  // producers + consumers
   p.threads = threads;
 
@@ -362,8 +367,38 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   return LFBP_OK;
 }
 
-int launch(const HpPlan& p, const void* src, void* dst, cudaStream_t st) {
-  if (p.n_units == 0) return LFBP_OK;
+// Ticket counters of HP_FLAG_DYNAMIC launches: a ring of slots per device,
+// each zeroed on the launch's own stream right before the launch, so
+// stream order alone makes it correct (launches in flight at once on
+// different streams get different slots while fewer than kCounterSlots).
+constexpr int kCounterSlots = 1024;
+std::mutex g_ctr_mu;
+std::map<int, unsigned long long*> g_ctr_pool;
+std::atomic<uint32_t> g_ctr_next{0};
+
+int counter_slot(unsigned long long** out) {
+  int dev = 0;
+  HP_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ctr_mu);
+  auto it = g_ctr_pool.find(dev);
+  if (it == g_ctr_pool.end()) {
+    unsigned long long* p = nullptr;
+    HP_CUDA(cudaMalloc(&p, kCounterSlots * 128));
+    it = g_ctr_pool.emplace(dev, p).first;
+  }
+  // one 128-byte line per slot
+  *out = it->second + 16 * (g_ctr_next.fetch_add(1, std::memory_order_relaxed) % kCounterSlots);
+  return LFBP_OK;
+}
+
+int launch_one(const HpPlan& p0, const void* src, void* dst, cudaStream_t st) {
+  if (p0.n_units == 0) return LFBP_OK;
+  HpPlan p = p0;
+  if (p.flags & HP_FLAG_DYNAMIC) {
+    int rc = counter_slot(&p.counter);
+    if (rc) return rc;
+    HP_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned long long), st));
+  }
   const uint8_t* s8 = static_cast<const uint8_t*>(src);
   uint8_t* d8 = static_cast<uint8_t*>(dst);
   const bool tasks = (p.flags & HP_FLAG_TASKS) != 0;
@@ -380,6 +415,32 @@ int launch(const HpPlan& p, const void* src, void* dst, cudaStream_t st) {
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   HP_CUDA(cudaGetLastError());
+  return LFBP_OK;
+}
+
+// HP_FLAG_ZCHUNK: one launch per slab of about kZChunkBytes moved (r+w).  The
+// persistent CTAs take units round-robin without synchronising, so in a long
+// launch they drift apart and the units in flight spread over more rows and
+// pages; on C5 a 22 ms launch falls from 6.35 to 5.6-5.8 TB/s that way
+// (profiles/r02_zchunk.jsonl).  Each launch starts them level again.
+constexpr int64_t kZChunkBytes = int64_t(12) << 30;
+
+int launch(const HpPlan& p, const void* src, void* dst, cudaStream_t st) {
+  if (!(p.flags & HP_FLAG_ZCHUNK)) return launch_one(p, src, dst, st);
+  const int64_t plane_rw = 2 * p.n_s * p.n_t * p.n_x * p.n_y * p.elem;
+  const int64_t want = int64_t(env_int("LFBP_ZCHUNK_MB", int(kZChunkBytes >> 20))) << 20;
+  const int64_t k = std::max<int64_t>(1, (want + plane_rw / 2) / plane_rw);
+  if (p.z_count <= k) return launch_one(p, src, dst, st);
+  const int64_t per_plane = p.n_units / p.z_count;
+  for (int64_t z = 0; z < p.z_count; z += k) {
+    HpPlan c = p;
+    c.z_begin = p.z_begin + z;
+    c.z_count = std::min<int64_t>(k, p.z_count - z);
+    c.n_units = per_plane * c.z_count;
+    c.grid = static_cast<int32_t>(std::min<int64_t>(p.grid, c.n_units));
+    int rc = launch_one(c, src, dst, st);
+    if (rc) return rc;
+  }
   return LFBP_OK;
 }
 
