@@ -164,6 +164,9 @@ const Knobs kCandidates[] = {
     // 6.35 TB/s on the whole C5 array (profiles/r02_zchunk.jsonl)
     {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ZCHUNK}, {3, 64, 8, 32, HP_FLAG_ZCHUNK},
     {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ZCHUNK, 145},
+    // dynamic unit tickets (HP_FLAG_DYNAMIC) hold the CTAs level inside one
+    // launch: C5 6.32 TB/s on all 148 SMs, C2 +0.5 % (profiles/r02_dynamic_ab.jsonl)
+    {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_DYNAMIC}, {2, 96, 12, 0, HP_FLAG_TASKS | HP_FLAG_DYNAMIC},
     // the (row, phase-class) task consumer: C3 +3-5 %, C2 J = 8 on par
     // (profiles/r02_tasks_ab.jsonl)
     {4, 48, 12, 0, HP_FLAG_TASKS}, {2, 96, 12, 0, HP_FLAG_TASKS},

@@ -197,6 +197,13 @@ ORDER_SHAPES = [
     {"LFBP_KFLAGS": "16"}, {"LFBP_KFLAGS": "24", "LFBP_STAGE_MAX_KB": "2"},
     {"LFBP_KFLAGS": "24", "LFBP_STAGE_KB": "200", "LFBP_STAGE_MAX_KB": "200"},
     {"LFBP_KFLAGS": "8", "LFBP_GRID": "37", "LFBP_CONSUMER_WARPS": "3"}, {"LFBP_KFLAGS": "0", "LFBP_GRID": "140"},
+    # round 2: task consumer, z-chunked launches (1 MB chunks: one launch per
+    # plane or so), dynamic unit tickets, and their combinations
+    {"LFBP_KFLAGS": "32"}, {"LFBP_KFLAGS": "32", "LFBP_STAGE_MAX_KB": "2"},
+    {"LFBP_KFLAGS": "40", "LFBP_CONSUMER_WARPS": "3", "LFBP_STAGES": "2"},
+    {"LFBP_KFLAGS": "64", "LFBP_ZCHUNK_MB": "1"}, {"LFBP_KFLAGS": "72", "LFBP_ZCHUNK_MB": "1", "LFBP_GRID": "145"},
+    {"LFBP_KFLAGS": "128"}, {"LFBP_KFLAGS": "136", "LFBP_CONSUMER_WARPS": "3", "LFBP_GRID": "5"},
+    {"LFBP_KFLAGS": "160"}, {"LFBP_KFLAGS": "200", "LFBP_ZCHUNK_MB": "1", "LFBP_STAGE_MAX_KB": "2"},
 ])
 @pytest.mark.parametrize("shape,dtype", ORDER_SHAPES)
 def test_unit_orders_are_bit_exact(monkeypatch, env, shape, dtype):
@@ -210,7 +217,10 @@ def test_unit_orders_are_bit_exact(monkeypatch, env, shape, dtype):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     p = plan(shape, dtype)
-    assert p["flags"] == int(env["LFBP_KFLAGS"])
+    want = int(env["LFBP_KFLAGS"])
+    if p["producers"] > 1:
+        want &= ~128   # dynamic tickets need the one-producer-warp plan
+    assert p["flags"] == want
     H = random_psf_like_reference(shape, density=0.9, seed=sum(shape) + 3, dtype=dtype)
     out = hprime_device(to_device(H))
     torch.cuda.synchronize()
@@ -423,7 +433,8 @@ def test_autotuner_picks_a_candidate_and_stays_exact(monkeypatch):
     torch = _torch()
     from paper_2003_09133_b200 import f_order_empty, hprime_device, plan, plan_candidates
     from paper_2003_09133_b200.verify import compare_device
-    for k in ("LFBP_STAGES", "LFBP_STAGE_KB", "LFBP_CONSUMER_WARPS", "LFBP_SUBWARP", "LFBP_AUTOTUNE"):
+    for k in ("LFBP_STAGES", "LFBP_STAGE_KB", "LFBP_CONSUMER_WARPS", "LFBP_SUBWARP", "LFBP_AUTOTUNE",
+              "LFBP_KFLAGS", "LFBP_GRID", "LFBP_ZCHUNK_MB"):
         monkeypatch.delenv(k, raising=False)
     shape = (197, 193, 15, 13, 5)               # a plane shape no other test tunes; 2 x 190 MB moved
     src = f_order_empty(shape, torch.float32)
