@@ -104,9 +104,11 @@ int lfbp_tune(const int64_t dims[5], int dtype, int device, int64_t z_count);
 /* The autotuner's candidate plans for size class 1 (launches moving
  * >= 256 MB) or 0 (8-256 MB): writes up to `max_n` records of 6 int32
  * (smem stages, stage KB, consumer warps, lanes per row -- 0 = by row
- * length --, unit-order flags -- 8 = along y' diagonals, 16 = rotated run /
- * row order --, SMs used -- 0 = all) into `knobs` (may be NULL) and returns
- * the number of candidates.  No GPU. */
+ * length --, flags -- 8 = unit order along y' diagonals, 16 = rotated run /
+ * row order, 32 = (row, phase-class) task consumer, 64 = one launch per
+ * ~12 GB z-slab, 128 = units handed out by a per-launch ticket counter --,
+ * SMs used -- 0 = all) into `knobs` (may be NULL) and returns the number of
+ * candidates.  No GPU. */
 int lfbp_plan_candidates(int size_class, int32_t* knobs, int max_n);
 
 /* memcpy of `bytes` split over `threads` host threads (<= 0: the library's

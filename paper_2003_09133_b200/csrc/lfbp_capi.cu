@@ -70,6 +70,15 @@ struct DevProps {
   bool real = false;
 };
 
+// Ticket counters of HP_FLAG_DYNAMIC launches: a ring of slots per device,
+// each zeroed on the launch's own stream right before the launch, so
+// stream order alone makes it correct (launches in flight at once on
+// different streams get different slots while fewer than kCounterSlots).
+constexpr int kCounterSlots = 1024;
+std::mutex g_ctr_mu;
+std::map<int, unsigned long long*> g_ctr_pool;
+std::atomic<uint32_t> g_ctr_next{0};
+
 std::mutex g_props_mu;
 std::map<int, DevProps> g_props;
 
@@ -91,6 +100,12 @@ DevProps device_props(int dev) {
     cudaFuncSetAttribute(hp::hprime_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
     cudaFuncSetAttribute(hp::hprime_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
     cudaFuncSetAttribute(hp::hprime_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem_optin);
+    {  // the ticket-counter ring, allocated here so that no launch (or stream
+       // capture) ever has to allocate
+      std::lock_guard<std::mutex> lk2(g_ctr_mu);
+      unsigned long long* c = nullptr;
+      if (!g_ctr_pool.count(dev) && cudaMalloc(&c, kCounterSlots * 128) == cudaSuccess) g_ctr_pool[dev] = c;
+    }
     cudaSetDevice(cur);
   } else {
     cudaGetLastError();  // clear "no device" state
@@ -370,14 +385,6 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   return LFBP_OK;
 }
 
-// Ticket counters of HP_FLAG_DYNAMIC launches: a ring of slots per device,
-// each zeroed on the launch's own stream right before the launch, so
-// stream order alone makes it correct (launches in flight at once on
-// different streams get different slots while fewer than kCounterSlots).
-constexpr int kCounterSlots = 1024;
-std::mutex g_ctr_mu;
-std::map<int, unsigned long long*> g_ctr_pool;
-std::atomic<uint32_t> g_ctr_next{0};
 
 int counter_slot(unsigned long long** out) {
   int dev = 0;
