@@ -24,6 +24,35 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// HP_CHECKED builds (tools/build_variant.sh CHECKED -DHP_CHECKED): every
+// shared-memory load and global store is bounds-checked, and the ring
+// protocol is checked (a stage's unit must not change while its consumers
+// use it).  compute-sanitizer is unavailable on the GPU pool; this build
+// plus the fuzz sweep stands in for memcheck / racecheck.
+#if defined(HP_CHECKED)
+__shared__ const uint8_t* hp_chk_dst;
+__shared__ unsigned long long hp_chk_bytes;
+__device__ __forceinline__ uint32_t dyn_smem_size() {
+  uint32_t v;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
+#define HP_CHECK(cond, what)                                                                    \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("HP_CHECKED: %s failed (block %d thread %d)\n", what, blockIdx.x, threadIdx.x);    \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#define HP_CHECK_STORE(ptr, bytes)                                                              \
+  HP_CHECK(reinterpret_cast<const uint8_t*>(ptr) >= hp_chk_dst &&                               \
+               reinterpret_cast<const uint8_t*>(ptr) + (bytes) <= hp_chk_dst + hp_chk_bytes,    \
+           "global store in bounds")
+#else
+#define HP_CHECK(cond, what) ((void)0)
+#define HP_CHECK_STORE(ptr, bytes) ((void)0)
+#endif
+
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
@@ -34,6 +63,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#if defined(HP_WAIT_HINT)  // experiment builds: suspend-time hint (ns) instead of the default poll window
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "HP_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra HP_WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity), "r"(HP_WAIT_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -43,6 +83,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void fence_barrier_init() {
@@ -86,6 +127,7 @@ struct UnitHdr {
   int32_t next_row;     // work counter: consumer warps claim rows with atomicAdd
   int32_t rot;          // HP_FLAG_ROTATE: rows are claimed starting at this one
   int32_t stop;         // HP_FLAG_DYNAMIC: no unit in this stage, the consumers exit
+  uint32_t unit;        // the unit index (ring-protocol checks of HP_CHECKED builds)
 };
 constexpr int kHdrBytes = 64;
 
@@ -238,6 +280,7 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
     h->next_row = 0;
     h->rot = (p.flags & HP_FLAG_ROTATE) ? static_cast<int32_t>(u % static_cast<uint32_t>(w.jb * p.n_x)) : 0;
     h->stop = 0;
+    h->unit = u;
   }
   tx = __reduce_add_sync(0xffffffffu, tx);
   __syncwarp();                                    // header and tail stores before the release
@@ -246,6 +289,13 @@ __device__ __forceinline__ void issue_unit(const HpPlan& p, const uint8_t* __res
 
 template <int E>
 __device__ __forceinline__ typename Word<E>::T lds(uint32_t addr) {
+#if defined(HP_CHECKED)
+  {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t lo = smem_u32(smem) + 128;
+    HP_CHECK(addr >= lo && addr + E <= smem_u32(smem) + dyn_smem_size(), "shared load in bounds");
+  }
+#endif
   if constexpr (E == 4) {
     uint32_t v;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -259,6 +309,8 @@ __device__ __forceinline__ typename Word<E>::T lds(uint32_t addr) {
 
 template <int E>
 __device__ __forceinline__ void st_vec(typename Word<E>::T* dst, const typename Word<E>::T* v) {
+  HP_CHECK_STORE(dst, 16);
+  HP_CHECK((reinterpret_cast<uintptr_t>(dst) & 15) == 0, "16-byte store aligned");
 #if defined(HP_ST_VARIANT) && HP_ST_VARIANT == 1  // experiment builds: streaming-store hints
   if constexpr (E == 4)
     asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(v[0]), "r"(v[1]), "r"(v[2]),
@@ -354,7 +406,10 @@ __device__ __forceinline__ void row_groups(typename Word<E>::T* o, int32_t g, in
     load_group<E, WRAP1>(v, a0, x0, n_x, step, nr);
 #pragma unroll
     for (int q = 0; q < VE; ++q)
-      if (i0 + q >= i_lo && i0 + q < i_end) o[q] = v[q];
+      if (i0 + q >= i_lo && i0 + q < i_end) {
+        HP_CHECK_STORE(o + q, E);
+        o[q] = v[q];
+      }
   };
   if (i0 < i_lo) {  // leading partial group (g == 0)
     masked();
@@ -452,9 +507,15 @@ __device__ __forceinline__ void consume_unit(const HpPlan& p, uint8_t* __restric
     const int32_t o_in = n_s * j + xs * (xp + n_x * yp);
     T* orow = dz + o_in;
     if (zero_row) {
-      for (int32_t i = i_lo + sl; i < h.i_hi; i += W) orow[i] = T(0);
+      for (int32_t i = i_lo + sl; i < h.i_hi; i += W) {
+        HP_CHECK_STORE(orow + i, E);
+        orow[i] = T(0);
+      }
     } else {
-      if (i_end < h.i_hi && sl == 0) orow[n_s - 1] = T(0);  // even n_s: row i = n_s - 1 is zero
+      if (i_end < h.i_hi && sl == 0) {  // even n_s: row i = n_s - 1 is zero
+        HP_CHECK_STORE(orow + n_s - 1, E);
+        orow[n_s - 1] = T(0);
+      }
       const int32_t gs = i_lo - ((o_in + zmis + i_lo) & (VE - 1));   // first group start (element i)
       const int32_t ng = i_end > i_lo ? (i_end - gs + VE - 1) / VE : 0;
       int32_t g = sl;
@@ -531,7 +592,10 @@ __device__ __forceinline__ void consume_unit_tasks(const HpPlan& p, uint8_t* __r
     const int32_t yp = zero_row ? h.y : static_cast<int32_t>(hp_mod(p.ny_div, static_cast<uint32_t>(h.y + t + p.ny_off)));
     const int32_t o_in = n_s * j + xs * (xp + n_x * yp);
     T* orow = dz + o_in;
-    if (c == 0 && i_end < i_hi) orow[n_s - 1] = T(0);  // even n_s: row i = n_s - 1 is zero
+    if (c == 0 && i_end < i_hi) {  // even n_s: row i = n_s - 1 is zero
+      HP_CHECK_STORE(orow + n_s - 1, E);
+      orow[n_s - 1] = T(0);
+    }
     const int32_t gs = i_lo - ((o_in + zmis + i_lo) & (VE - 1));   // first group start (element i)
     const int32_t ng = i_end > i_lo ? (i_end - gs + VE - 1) / VE : 0;
     if (c >= ng) continue;
@@ -545,7 +609,10 @@ __device__ __forceinline__ void consume_unit_tasks(const HpPlan& p, uint8_t* __r
 #pragma unroll
         for (int q = 0; q < VE; ++q) {
           const int32_t i = i0 + m * ostep + q;
-          if (i >= i_lo && i < i_end) o[m * ostep + q] = T(0);
+          if (i >= i_lo && i < i_end) {
+            HP_CHECK_STORE(o + m * ostep + q, E);
+            o[m * ostep + q] = T(0);
+          }
         }
       continue;
     }
@@ -563,7 +630,10 @@ __device__ __forceinline__ void consume_unit_tasks(const HpPlan& p, uint8_t* __r
 #pragma unroll
       for (int q = 0; q < VE; ++q) {
         const int32_t i = i0 + m * ostep + q;
-        if (i >= i_lo && i < i_end) o[m * ostep + q] = lds<E>(A[q] - off);
+        if (i >= i_lo && i < i_end) {
+          HP_CHECK_STORE(o + m * ostep + q, E);
+          o[m * ostep + q] = lds<E>(A[q] - off);
+        }
       }
     };
     const int32_t m0 = head ? 1 : 0;
@@ -628,6 +698,12 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = p.producers;
   const int nc = (blockDim.x >> 5) - np;
+#if defined(HP_CHECKED)
+  if (threadIdx.x == 0) {
+    hp_chk_dst = dst;
+    hp_chk_bytes = static_cast<unsigned long long>(p.total_bytes);
+  }
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(smem_u32(&full[s]), np);
@@ -694,11 +770,17 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
     mbar_wait(smem_u32(&full[st]), ph);
     const uint8_t* stage = stages + static_cast<int64_t>(st) * p.stage_bytes;
     if (dynamic && reinterpret_cast<const volatile UnitHdr*>(stage)->stop) break;
+#if defined(HP_CHECKED)
+    const uint32_t unit_in = reinterpret_cast<const volatile UnitHdr*>(stage)->unit;
+    HP_CHECK(dynamic || unit_in == first + k * stride, "stage holds this warp's next unit");
+    HP_CHECK(unit_in < n_units, "unit index in range");
+#endif
     if constexpr (TASKS)
       consume_unit_tasks<E>(p, dst, stage, stage0 + static_cast<uint32_t>(st) * p.stage_bytes, lane);
     else
       consume_unit<E>(p, dst, stage, stage0 + static_cast<uint32_t>(st) * p.stage_bytes, warp - np, nc, lane);
     __syncwarp();
+    HP_CHECK(reinterpret_cast<const volatile UnitHdr*>(stage)->unit == unit_in, "stage not refilled while in use");
     if (lane == 0) mbar_arrive(smem_u32(&empty[st]));
     if (++st == S) {
       st = 0;

@@ -28,10 +28,12 @@ def main():
     shapes = [((55, 55, 11, 11, 2), np.float32), ((27, 20, 13, 5, 2), np.float64), ((66, 41, 21, 9, 1), np.float32),
               ((5, 3, 3, 3, 1), np.float32), ((8, 12, 7, 3, 3), np.float32), ((1, 1, 1, 1, 3), np.float64)]
     envs = [{}, {"LFBP_STAGE_MAX_KB": "2"}, {"LFBP_STAGES": "1"}, {"LFBP_SUBWARP": "32", "LFBP_CONSUMER_WARPS": "3"},
-            {"LFBP_STAGE_KB": "1", "LFBP_SUBWARP": "8"}]
+            {"LFBP_STAGE_KB": "1", "LFBP_SUBWARP": "8"}, {"LFBP_KFLAGS": "32"},
+            {"LFBP_KFLAGS": "160", "LFBP_CONSUMER_WARPS": "3"}, {"LFBP_KFLAGS": "200", "LFBP_ZCHUNK_MB": "1"}]
     n = 0
     for env in envs:
-        for k in ("LFBP_STAGE_MAX_KB", "LFBP_STAGES", "LFBP_SUBWARP", "LFBP_CONSUMER_WARPS", "LFBP_STAGE_KB"):
+        for k in ("LFBP_STAGE_MAX_KB", "LFBP_STAGES", "LFBP_SUBWARP", "LFBP_CONSUMER_WARPS", "LFBP_STAGE_KB",
+                  "LFBP_KFLAGS", "LFBP_ZCHUNK_MB"):
             os.environ.pop(k, None)
         os.environ.update(env)
         for shape, dt in shapes:
