@@ -63,17 +63,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-#if defined(HP_WAIT_HINT)  // experiment builds: suspend-time hint (ns) instead of the default poll window
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "HP_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra HP_WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity), "r"(HP_WAIT_HINT)
-      : "memory");
-#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -83,7 +72,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "}\n" ::"r"(bar),
       "r"(parity)
       : "memory");
-#endif
 }
 
 __device__ __forceinline__ void fence_barrier_init() {

@@ -91,6 +91,9 @@ DevProps device_props(int dev) {
   if (dev >= 0 && cudaGetDeviceCount(&n) == cudaSuccess && dev < n) {
     cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+#if defined(HP_CHECKED)
+    p.smem_optin -= 1024;  // the checked build's static shared variables
+#endif
     cudaDeviceGetAttribute(&p.max_threads_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
     p.real = true;
     int cur = 0;
