@@ -197,3 +197,28 @@ def test_plan_candidates_are_exported():
     assert all(len(k) == 6 and k[0] >= 1 and k[1] >= 1 and k[2] >= 1 for k in large + small)
     assert len(set(large)) == len(large)
     assert _native.lib().lfbp_plan_candidates(7, None, 0) < 0
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C4", "C5"])
+def test_round2_plan_flags(monkeypatch, cfg):
+    """Planner side of the round-2 kernel options (no GPU): the task consumer
+    stages runs at a 16-byte row pitch; z-chunked and dynamic-ticket plans
+    keep their flags (dynamic only with one producer warp); the tuner's
+    candidate list holds each of them."""
+    from paper_2003_09133_b200 import plan, plan_candidates
+    from paper_2003_09133_b200.configs import WORKLOADS
+    w = WORKLOADS[cfg]
+    base = plan(w.shape, w.dtype)
+    assert base["row_pitch"] % 16 == (w.shape[0] * w.shape[1] * w.itemsize) % 16
+    monkeypatch.setenv("LFBP_KFLAGS", "32")
+    p = plan(w.shape, w.dtype)
+    assert p["flags"] == 32 and p["row_pitch"] % 16 == 0
+    assert p["row_pitch"] >= p["J"] * w.shape[0] * w.itemsize + 32
+    assert p["stage_bytes"] >= 64 + 16 + w.shape[2] * p["row_pitch"]
+    for f in (64, 128, 200):
+        monkeypatch.setenv("LFBP_KFLAGS", str(f))
+        assert plan(w.shape, w.dtype)["flags"] == f
+    monkeypatch.setenv("LFBP_KFLAGS", "128")
+    assert plan((181, 181, 95, 55, 1))["flags"] == 0   # three producer warps: no tickets
+    flags = {k[4] for k in plan_candidates(1)}
+    assert {32 | 128, 8 | 64, 8 | 128} <= flags
