@@ -185,6 +185,11 @@ const Knobs kCandidates[] = {
     // dynamic unit tickets (HP_FLAG_DYNAMIC) hold the CTAs level inside one
     // launch: C5 6.32 TB/s on all 148 SMs, C2 +0.5 % (profiles/r02_dynamic_ab.jsonl)
     {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_DYNAMIC}, {2, 96, 12, 0, HP_FLAG_TASKS | HP_FLAG_DYNAMIC},
+    // with tickets, narrow bands and 8-lane rows, also several CTAs per SM:
+    // C2 6563 GB/s (J = 4), C3 6427 (J = 1, 3 CTAs per SM), from a 480-plan
+    // sweep (profiles/r02_sweep_c2_c3_row.jsonl)
+    {4, 48, 12, 8, HP_FLAG_DYNAMIC}, {4, 64, 12, 8, HP_FLAG_DYNAMIC}, {2, 32, 8, 8, HP_FLAG_DYNAMIC},
+    {3, 32, 8, 8, HP_FLAG_DYNAMIC}, {3, 64, 12, 16, HP_FLAG_DYNAMIC}, {4, 32, 8, 8, HP_FLAG_DYNAMIC},
     // the (row, phase-class) task consumer: C3 +3-5 %, C2 J = 8 on par
     // (profiles/r02_tasks_ab.jsonl)
     {4, 48, 12, 0, HP_FLAG_TASKS}, {2, 96, 12, 0, HP_FLAG_TASKS},
