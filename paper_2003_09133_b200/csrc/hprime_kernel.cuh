@@ -708,28 +708,36 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
     if (dynamic) {
       // units are handed out in global order by one counter per launch, so
       // the units in flight always form one window of ~grid * stages units
-      // and no CTA drifts ahead of the others; the next ticket is fetched
-      // while the current unit is issued
+      // and no CTA drifts ahead of the others; producer warp 0 fetches the
+      // next ticket while the current unit is issued and, with several
+      // producer warps, passes it on through the stage header (named
+      // barrier 1 over the producer warps)
       unsigned long long* ctr = p.counter;
       uint32_t u = 0, nxt = 0;
-      if (lane == 0) u = static_cast<uint32_t>(atomicAdd(ctr, 1ull));
-      u = __shfl_sync(0xffffffffu, u, 0);
+      if (warp == 0 && lane == 0) u = static_cast<uint32_t>(atomicAdd(ctr, 1ull));
       for (uint32_t k = 0;; ++k) {
         if (k >= static_cast<uint32_t>(S)) {
           mbar_wait(smem_u32(&empty[st]), ph ^ 1u);
           fence_proxy_async_smem();
         }
         uint8_t* stage = stages + static_cast<int64_t>(st) * p.stage_bytes;
+        if (np == 1) {
+          u = __shfl_sync(0xffffffffu, u, 0);
+        } else {
+          if (warp == 0 && lane == 0) reinterpret_cast<volatile UnitHdr*>(stage)->unit = u;
+          asm volatile("bar.sync 1, %0;" ::"r"(32 * np) : "memory");
+          u = reinterpret_cast<volatile UnitHdr*>(stage)->unit;
+          asm volatile("bar.sync 1, %0;" ::"r"(32 * np) : "memory");
+        }
         if (u >= n_units) {
-          if (lane == 0) {
-            reinterpret_cast<UnitHdr*>(stage)->stop = 1;
-            mbar_arrive_expect_tx(smem_u32(&full[st]), 0);
-          }
+          if (warp == 0 && lane == 0) reinterpret_cast<UnitHdr*>(stage)->stop = 1;
+          __syncwarp();
+          if (lane == 0) mbar_arrive_expect_tx(smem_u32(&full[st]), 0);
           break;
         }
-        if (lane == 0) nxt = static_cast<uint32_t>(atomicAdd(ctr, 1ull));
+        if (warp == 0 && lane == 0) nxt = static_cast<uint32_t>(atomicAdd(ctr, 1ull));
         issue_unit<E, TASKS>(p, src, u, stage, smem_u32(&full[st]), lane, warp, policy);
-        u = __shfl_sync(0xffffffffu, nxt, 0);
+        u = nxt;
         if (++st == S) {
           st = 0;
           ph ^= 1u;

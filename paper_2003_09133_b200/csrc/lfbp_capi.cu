@@ -341,7 +341,6 @@ int make_plan(HpPlan& p, const int64_t d[5], int E, int64_t z_begin, int64_t z_c
   int prod = env_int("LFBP_PRODUCERS", int((d[2] + 31) / 32));
   prod = std::max(1, std::min(prod, 17 - cwarps));
   p.producers = prod;
-  if (prod > 1) p.flags &= ~HP_FLAG_DYNAMIC;  // the ticket is taken by the one producer warp
   const int threads = 32 * (prod + cwarps);  // producers + consumers
   p.threads = threads;
 

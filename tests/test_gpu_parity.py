@@ -204,6 +204,8 @@ ORDER_SHAPES = [
     {"LFBP_KFLAGS": "64", "LFBP_ZCHUNK_MB": "1"}, {"LFBP_KFLAGS": "72", "LFBP_ZCHUNK_MB": "1", "LFBP_GRID": "145"},
     {"LFBP_KFLAGS": "128"}, {"LFBP_KFLAGS": "136", "LFBP_CONSUMER_WARPS": "3", "LFBP_GRID": "5"},
     {"LFBP_KFLAGS": "160"}, {"LFBP_KFLAGS": "200", "LFBP_ZCHUNK_MB": "1", "LFBP_STAGE_MAX_KB": "2"},
+    {"LFBP_KFLAGS": "128", "LFBP_PRODUCERS": "3"},   # several producer warps share each ticket
+    {"LFBP_KFLAGS": "160", "LFBP_PRODUCERS": "2", "LFBP_STAGE_MAX_KB": "2"},
 ])
 @pytest.mark.parametrize("shape,dtype", ORDER_SHAPES)
 def test_unit_orders_are_bit_exact(monkeypatch, env, shape, dtype):
@@ -217,10 +219,7 @@ def test_unit_orders_are_bit_exact(monkeypatch, env, shape, dtype):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     p = plan(shape, dtype)
-    want = int(env["LFBP_KFLAGS"])
-    if p["producers"] > 1:
-        want &= ~128   # dynamic tickets need the one-producer-warp plan
-    assert p["flags"] == want
+    assert p["flags"] == int(env["LFBP_KFLAGS"])
     H = random_psf_like_reference(shape, density=0.9, seed=sum(shape) + 3, dtype=dtype)
     out = hprime_device(to_device(H))
     torch.cuda.synchronize()

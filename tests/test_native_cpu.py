@@ -203,7 +203,7 @@ def test_plan_candidates_are_exported():
 def test_round2_plan_flags(monkeypatch, cfg):
     """Planner side of the round-2 kernel options (no GPU): the task consumer
     stages runs at a 16-byte row pitch; z-chunked and dynamic-ticket plans
-    keep their flags (dynamic only with one producer warp); the tuner's
+    keep their flags (also with several producer warps); the tuner's
     candidate list holds each of them."""
     from paper_2003_09133_b200 import plan, plan_candidates
     from paper_2003_09133_b200.configs import WORKLOADS
@@ -219,6 +219,7 @@ def test_round2_plan_flags(monkeypatch, cfg):
         monkeypatch.setenv("LFBP_KFLAGS", str(f))
         assert plan(w.shape, w.dtype)["flags"] == f
     monkeypatch.setenv("LFBP_KFLAGS", "128")
-    assert plan((181, 181, 95, 55, 1))["flags"] == 0   # three producer warps: no tickets
+    wide = plan((181, 181, 95, 55, 1))     # three producer warps share each ticket
+    assert wide["flags"] == 128 and wide["producers"] == 3
     flags = {k[4] for k in plan_candidates(1)}
     assert {32 | 128, 8 | 64, 8 | 128} <= flags
