@@ -1,6 +1,6 @@
 """Kernel tuning sweep on the GPU box (timing only; parity lives in tests/).
 
-    python tools/sweep.py --configs C2,C4 [--grid default|wide] [--reps 20]
+    python tools/sweep.py --configs C2,C4,181x181x95x55x11 [--grid default|wide] [--reps 20]
 
 Inputs are filled on the device (torch.rand) -- values do not affect a copy
 kernel.  The plan knobs are environment variables read by the C-ABI planner
@@ -35,8 +35,16 @@ def main():
     spec = [kv.split("=") for kv in a.grid.split(";")]
     keys = tuple("LFBP_" + k for k, _ in spec)
     grid = list(itertools.product(*[[int(v) for v in vs.split(",")] for _, vs in spec]))
+    class _Shape:  # "181x181x95x55x11" (f32) instead of a BASELINE config name
+        def __init__(self, spec):
+            import numpy as np
+            self.shape = tuple(int(v) for v in spec.split("x"))
+            self.dtype = np.float32
+            self.itemsize = 4
+            self.nbytes = int(np.prod(self.shape)) * 4
+
     for cfg in a.configs.split(","):
-        w = WORKLOADS[cfg]
+        w = WORKLOADS[cfg] if cfg in WORKLOADS else _Shape(cfg)
         tdt = torch.float32 if w.itemsize == 4 else torch.float64
         src = f_order_empty(w.shape, tdt)
         src.permute(4, 3, 2, 1, 0).reshape(-1).uniform_()
