@@ -679,7 +679,9 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
   uint64_t* empty = full + 8;
   uint8_t* stages = smem + 128;
   const uint32_t first = blockIdx.x, stride = gridDim.x;
-  if (first >= p.n_units) return;
+  // (the planner keeps grid <= n_units; with HP_FLAG_DYNAMIC every CTA must
+  // take part in the ticket slot's reset count)
+  if (first >= p.n_units && !(p.flags & HP_FLAG_DYNAMIC)) return;
   const uint32_t n_units = static_cast<uint32_t>(p.n_units);
   const uint32_t mine = (n_units - first + stride - 1) / stride;
   const int S = p.stages;
@@ -730,7 +732,15 @@ __global__ void __launch_bounds__(544, 1) hprime_kernel(const HpPlan p, const ui
           asm volatile("bar.sync 1, %0;" ::"r"(32 * np) : "memory");
         }
         if (u >= n_units) {
-          if (warp == 0 && lane == 0) reinterpret_cast<UnitHdr*>(stage)->stop = 1;
+          if (warp == 0 && lane == 0) {
+            reinterpret_cast<UnitHdr*>(stage)->stop = 1;
+            // this CTA takes no more tickets; the last CTA to get here zeroes
+            // the slot for its next launch (no memset on the stream)
+            if (atomicAdd(ctr + 1, 1ull) == static_cast<unsigned long long>(gridDim.x) - 1) {
+              atomicExch(ctr, 0ull);
+              atomicExch(ctr + 1, 0ull);
+            }
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive_expect_tx(smem_u32(&full[st]), 0);
           break;

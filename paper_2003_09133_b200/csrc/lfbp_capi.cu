@@ -70,10 +70,11 @@ struct DevProps {
   bool real = false;
 };
 
-// Ticket counters of HP_FLAG_DYNAMIC launches: a ring of slots per device,
-// each zeroed on the launch's own stream right before the launch, so
-// stream order alone makes it correct (launches in flight at once on
-// different streams get different slots while fewer than kCounterSlots).
+// Ticket counters of HP_FLAG_DYNAMIC launches: a ring of 128-byte slots per
+// device ([0] the ticket, [1] CTAs done), zeroed once at allocation; the last
+// CTA of a launch zeroes its slot again for the slot's next launch, so no
+// memset is queued per launch.  Launches in flight at once get different
+// slots as long as fewer than kCounterSlots are in flight.
 constexpr int kCounterSlots = 1024;
 std::mutex g_ctr_mu;
 std::map<int, unsigned long long*> g_ctr_pool;
@@ -107,7 +108,12 @@ DevProps device_props(int dev) {
        // capture) ever has to allocate
       std::lock_guard<std::mutex> lk2(g_ctr_mu);
       unsigned long long* c = nullptr;
-      if (!g_ctr_pool.count(dev) && cudaMalloc(&c, kCounterSlots * 128) == cudaSuccess) g_ctr_pool[dev] = c;
+      if (!g_ctr_pool.count(dev) && cudaMalloc(&c, kCounterSlots * 128) == cudaSuccess) {
+        if (cudaMemset(c, 0, kCounterSlots * 128) == cudaSuccess)
+          g_ctr_pool[dev] = c;
+        else
+          cudaFree(c);
+      }
     }
     cudaSetDevice(cur);
   } else {
@@ -401,6 +407,7 @@ int counter_slot(unsigned long long** out) {
   if (it == g_ctr_pool.end()) {
     unsigned long long* p = nullptr;
     HP_CUDA(cudaMalloc(&p, kCounterSlots * 128));
+    HP_CUDA(cudaMemset(p, 0, kCounterSlots * 128));
     it = g_ctr_pool.emplace(dev, p).first;
   }
   // one 128-byte line per slot
@@ -414,7 +421,6 @@ int launch_one(const HpPlan& p0, const void* src, void* dst, cudaStream_t st) {
   if (p.flags & HP_FLAG_DYNAMIC) {
     int rc = counter_slot(&p.counter);
     if (rc) return rc;
-    HP_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned long long), st));
   }
   const uint8_t* s8 = static_cast<const uint8_t*>(src);
   uint8_t* d8 = static_cast<uint8_t*>(dst);
