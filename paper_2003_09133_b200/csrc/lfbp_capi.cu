@@ -163,7 +163,10 @@ int tune_class(int64_t moved_bytes) {
 // fewer, busier consumer warps per CTA and more CTAs (C1: 14.5 vs 17 us).
 Knobs default_knobs(int64_t moved_bytes) {
   Knobs kn;
-  if (moved_bytes < kAutotuneMinBytes) kn.cwarps = 8;
+  if (moved_bytes < kAutotuneMinBytes)
+    kn.cwarps = 8;
+  else
+    kn.flags = HP_FLAG_DYNAMIC;  // level CTAs: the tuned plans of C2-C5 all take tickets
   return kn;
 }
 
@@ -206,6 +209,8 @@ const Knobs kCandidates[] = {
 const Knobs kSmallCandidates[] = {
     {4, 48, 8, 0}, {4, 16, 8, 0}, {4, 16, 4, 4}, {4, 8, 8, 4},
     {4, 24, 8, 0}, {4, 32, 8, 0}, {4, 12, 4, 4}, {4, 16, 8, 8},
+    {4, 48, 8, 0, HP_FLAG_DYNAMIC}, {4, 16, 8, 0, HP_FLAG_DYNAMIC}, {4, 24, 8, 0, HP_FLAG_DYNAMIC},
+    {4, 16, 4, 4, HP_FLAG_DYNAMIC},
 };
 constexpr int kNumCandidates = int(sizeof(kCandidates) / sizeof(kCandidates[0]));
 constexpr int kNumSmallCandidates = int(sizeof(kSmallCandidates) / sizeof(kSmallCandidates[0]));
