@@ -77,10 +77,13 @@ int64_t lfbp_dropped_source_count(const int64_t dims[5]);
  * Asynchronous on `stream`; the caller synchronises -- except the FIRST call
  * for a plane shape / element size / device / size class (launches moving
  * >= 8 MB) with no tuned plan: that call runs the autotuner on `src`/`dst`
- * first (40-60 timed launches with host synchronisations on `stream`; about
- * 1.4 s on C5) and so returns only after they finish.  Call lfbp_tune()
- * beforehand to keep every call asynchronous; LFBP_AUTOTUNE=0 disables the
- * tuner (untuned default plan). */
+ * first (about 40 candidate plans x 4 timed rounds with host
+ * synchronisations on `stream`; about 3.5 s on C5) and so returns only after
+ * they finish.  Call lfbp_tune() beforehand to keep every call asynchronous;
+ * LFBP_AUTOTUNE=0 disables the tuner (untuned default plan).  Plans with
+ * unit tickets (flag 128) take a counter slot from a per-device ring of 1024
+ * per launch; a captured CUDA graph reuses its slot on every replay, so one
+ * graph must not be replayed concurrently with itself. */
 int lfbp_hprime_device(const void* src, void* dst, const int64_t dims[5], int dtype, int inverse,
                        int64_t z_begin, int64_t z_end, void* stream);
 
