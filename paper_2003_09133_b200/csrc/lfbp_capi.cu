@@ -199,6 +199,9 @@ const Knobs kCandidates[] = {
     // sweep (profiles/r02_sweep_c2_c3_row.jsonl)
     {4, 48, 12, 8, HP_FLAG_DYNAMIC}, {4, 64, 12, 8, HP_FLAG_DYNAMIC}, {2, 32, 8, 8, HP_FLAG_DYNAMIC},
     {3, 32, 8, 8, HP_FLAG_DYNAMIC}, {3, 64, 12, 16, HP_FLAG_DYNAMIC}, {4, 32, 8, 8, HP_FLAG_DYNAMIC},
+    // C5 with tickets: the diagonal order on the full grid leads (6.42-6.45 TB/s;
+    // grid caps no longer help, profiles/r02_c5_tickets_sweep.jsonl)
+    {4, 48, 12, 8, HP_FLAG_DIAGONAL | HP_FLAG_DYNAMIC}, {4, 48, 8, 16, HP_FLAG_DYNAMIC},
     // the (row, phase-class) task consumer: C3 +3-5 %, C2 J = 8 on par
     // (profiles/r02_tasks_ab.jsonl)
     {4, 48, 12, 0, HP_FLAG_TASKS}, {2, 96, 12, 0, HP_FLAG_TASKS},
