@@ -98,15 +98,6 @@ __device__ __forceinline__ void st_v2_64(void* p, unsigned long long a, unsigned
   asm volatile("st.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
-__device__ __forceinline__ void st_v4_na(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.global.L1::no_allocate.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
-               : "memory");
-}
-
-__device__ __forceinline__ void st_v2_64_na(void* p, unsigned long long a, unsigned long long b) {
-  asm volatile("st.global.L1::no_allocate.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
-}
-
 // Decoded unit, written by the producer at the head of its stage so the
 // consumer warps read it with a few LDS instead of re-decoding.
 struct UnitHdr {
@@ -299,36 +290,10 @@ template <int E>
 __device__ __forceinline__ void st_vec(typename Word<E>::T* dst, const typename Word<E>::T* v) {
   HP_CHECK_STORE(dst, 16);
   HP_CHECK((reinterpret_cast<uintptr_t>(dst) & 15) == 0, "16-byte store aligned");
-#if defined(HP_ST_VARIANT) && HP_ST_VARIANT == 1  // experiment builds: streaming-store hints
-  if constexpr (E == 4)
-    asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(v[0]), "r"(v[1]), "r"(v[2]),
-                 "r"(v[3]) : "memory");
-  else
-    asm volatile("st.global.cs.v2.b64 [%0], {%1, %2};" ::"l"(dst), "l"(v[0]), "l"(v[1]) : "memory");
-#elif defined(HP_ST_VARIANT) && HP_ST_VARIANT == 2
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  if constexpr (E == 4)
-    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst), "r"(v[0]), "r"(v[1]),
-                 "r"(v[2]), "r"(v[3]), "l"(pol) : "memory");
-  else
-    asm volatile("st.global.L2::cache_hint.v2.b64 [%0], {%1, %2}, %3;" ::"l"(dst), "l"(v[0]), "l"(v[1]), "l"(pol)
-                 : "memory");
-#elif defined(HP_ST_VARIANT) && HP_ST_VARIANT == 3
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  if constexpr (E == 4)
-    asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst), "r"(v[0]), "r"(v[1]),
-                 "r"(v[2]), "r"(v[3]), "l"(pol) : "memory");
-  else
-    asm volatile("st.global.L2::cache_hint.v2.b64 [%0], {%1, %2}, %3;" ::"l"(dst), "l"(v[0]), "l"(v[1]), "l"(pol)
-                 : "memory");
-#else
   if constexpr (E == 4)
     st_v4(dst, v[0], v[1], v[2], v[3]);
   else
     st_v2_64(dst, v[0], v[1]);
-#endif
 }
 
 // Values of the VE elements of group g whose first element has source phase
