@@ -173,38 +173,23 @@ Knobs default_knobs(int64_t moved_bytes) {
 // Candidates tried by the autotuner (measured best plans of C1..C5 and
 // neighbours; every one is bit-exact, they differ only in speed).
 const Knobs kCandidates[] = {
-    {3, 48, 8, 8},  {4, 48, 12, 16}, {4, 48, 8, 8},  {4, 48, 8, 16}, {2, 96, 8, 16},
-    {3, 64, 8, 32}, {4, 48, 16, 16}, {2, 96, 8, 8},  {4, 16, 8, 0},  {4, 16, 4, 4},
-    {2, 96, 12, 32},  // C4 with the v7 loop: J = 3, +3 % over the former best (profiles/r01_sweep_v7.jsonl)
-    // long single-row units (C5): unit order along y' diagonals, rotated run /
-    // row order, and 140 of 148 SMs -- at full clock the 148-CTA y-fastest
-    // plan oversubscribes the memory system on some boxes (profiles/r02_*)
-    {3, 64, 8, 32, HP_FLAG_DIAGONAL}, {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ROTATE},
-    {3, 64, 8, 32, HP_FLAG_DIAGONAL, 140}, {3, 64, 8, 32, 0, 140}, {3, 64, 8, 32, HP_FLAG_ROTATE},
-    // C5 demand exceeds the DRAM supply with all 148 SMs and the rate collapses
-    // (5.94 TB/s); per SM it holds 44.8 GB/s up to 145 SMs: 6.45 TB/s there
-    // (profiles/r02_grid_sweep_fine.jsonl).  The cliff sits at a box-dependent
-    // SM count, so the tuner times both sides of it.
-    {3, 64, 8, 32, HP_FLAG_DIAGONAL, 144}, {3, 64, 8, 32, HP_FLAG_DIAGONAL, 145},
-    {4, 64, 8, 32, HP_FLAG_DIAGONAL, 146},
-    // ... and with ~12 GB launches (HP_FLAG_ZCHUNK) the full grid holds
-    // 6.35 TB/s on the whole C5 array (profiles/r02_zchunk.jsonl)
-    {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ZCHUNK}, {3, 64, 8, 32, HP_FLAG_ZCHUNK},
-    {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ZCHUNK, 145},
-    // dynamic unit tickets (HP_FLAG_DYNAMIC) hold the CTAs level inside one
-    // launch: C5 6.32 TB/s on all 148 SMs, C2 +0.5 % (profiles/r02_dynamic_ab.jsonl)
-    {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_DYNAMIC}, {2, 96, 12, 0, HP_FLAG_TASKS | HP_FLAG_DYNAMIC},
-    // with tickets, narrow bands and 8-lane rows, also several CTAs per SM:
-    // C2 6563 GB/s (J = 4), C3 6427 (J = 1, 3 CTAs per SM), from a 480-plan
-    // sweep (profiles/r02_sweep_c2_c3_row.jsonl)
+    // Dynamic unit tickets (HP_FLAG_DYNAMIC) hold the persistent CTAs level:
+    // every tuned C2-C5 plan since takes them (profiles/r02_dynamic_ab.jsonl,
+    // r02_sweep_c2_c3_row.jsonl, r02_c5_tickets_sweep.jsonl).  Narrow bands and
+    // 8-lane rows lead (C2 J = 4, C3 J = 1 with 3 CTAs per SM, C5 along y'
+    // diagonals); the task consumer draws less power and wins on the most
+    // power-limited boxes.
     {4, 48, 12, 8, HP_FLAG_DYNAMIC}, {4, 64, 12, 8, HP_FLAG_DYNAMIC}, {2, 32, 8, 8, HP_FLAG_DYNAMIC},
     {3, 32, 8, 8, HP_FLAG_DYNAMIC}, {3, 64, 12, 16, HP_FLAG_DYNAMIC}, {4, 32, 8, 8, HP_FLAG_DYNAMIC},
-    // C5 with tickets: the diagonal order on the full grid leads (6.42-6.45 TB/s;
-    // grid caps no longer help, profiles/r02_c5_tickets_sweep.jsonl)
-    {4, 48, 12, 8, HP_FLAG_DIAGONAL | HP_FLAG_DYNAMIC}, {4, 48, 8, 16, HP_FLAG_DYNAMIC},
-    // the (row, phase-class) task consumer: C3 +3-5 %, C2 J = 8 on par
-    // (profiles/r02_tasks_ab.jsonl)
-    {4, 48, 12, 0, HP_FLAG_TASKS}, {2, 96, 12, 0, HP_FLAG_TASKS},
+    {4, 48, 8, 16, HP_FLAG_DYNAMIC}, {4, 48, 12, 8, HP_FLAG_DIAGONAL | HP_FLAG_DYNAMIC},
+    {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_DYNAMIC}, {2, 96, 12, 0, HP_FLAG_TASKS | HP_FLAG_DYNAMIC},
+    // static round-robin plans, the round-1 bests (C2 {3,48,8,8}, C3 J = 3
+    // {2,96,12,32}, C4 and C5 {3,64,8,32}), and C5's best before tickets:
+    // diagonal order, ~12 GB launches (HP_FLAG_ZCHUNK), 145 of 148 SMs
+    // (profiles/r02_zchunk.jsonl, r02_grid_sweep_fine.jsonl)
+    {3, 48, 8, 8}, {4, 48, 12, 16}, {2, 96, 8, 8}, {3, 64, 8, 32}, {2, 96, 12, 32},
+    {4, 16, 8, 0}, {4, 16, 4, 4},
+    {3, 64, 8, 32, HP_FLAG_DIAGONAL | HP_FLAG_ZCHUNK, 145},
 };
 // Small problems (8-256 MB moved) are latency-bound: smaller stages (narrower
 // t-bands, several CTAs per SM) and short-row sub-warps; measured on the
