@@ -268,7 +268,7 @@ def test_wide_shape_default_plan_matches_oracle():
     from paper_2003_09133_b200.synth import random_psf_like_reference
     shape = (95, 95, 47, 37, 2)
     p = plan(shape)
-    assert p["producers"] == 2 and p["tile_y"] == 4
+    assert p["producers"] == 2 and p["tile_y"] == (1 if p["flags"] & 8 else 4)
     H = random_psf_like_reference(shape, density=0.8, seed=95, dtype=np.float32)
     out = hprime_device(to_device(H))
     torch.cuda.synchronize()
@@ -283,7 +283,8 @@ def test_reference_full_scale_acceptance_shape_involution():
     from paper_2003_09133_b200 import f_order_empty, plan
     from paper_2003_09133_b200.verify import involution_check
     shape = (181, 181, 95, 55, 1)
-    assert plan(shape)["producers"] == 3 and plan(shape)["tile_y"] == 4
+    p = plan(shape)   # untuned or tuned (an earlier test may have tuned this shape)
+    assert p["producers"] == 3 and p["tile_y"] == (1 if p["flags"] & 8 else 4)
     src = f_order_empty(shape, torch.float32)
     src.permute(4, 3, 2, 1, 0).reshape(-1).view(torch.int32).random_()
     assert involution_check(src) == (0, -1)
