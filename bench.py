@@ -248,7 +248,17 @@ def run_reference_processes(args, w, procs: int):
     ps = [ctx.Process(target=_ref_plane_worker, args=(w.name, z, args.steps, warm, bar, q)) for z in zs]
     for pr in ps:
         pr.start()
-    res = [q.get() for _ in ps]
+    res = []
+    import queue
+    while len(res) < len(ps):
+        try:
+            res.append(q.get(timeout=10))
+        except queue.Empty:
+            dead = [pr for pr in ps if pr.exitcode not in (None, 0)]
+            if dead:   # a worker died without reporting (e.g. the OOM killer)
+                for pr in ps:
+                    pr.kill()
+                raise RuntimeError(f"reference worker exited with code {dead[0].exitcode}")
     for pr in ps:
         pr.join()
     errs = [r[4] for r in res if r[4]]
