@@ -1,13 +1,17 @@
 // K1: the H -> H' rearrangement kernel for sm_100a.
 //
-// Persistent CTAs walk work units u = blockIdx.x + k * gridDim.x.  One
-// elected thread stages unit k + stages - 1 with 1-D bulk TMA
-// (cp.async.bulk global -> shared, completion on an mbarrier) while all
-// warps consume unit k from a ring of `stages` shared-memory buffers:
-// each output row is written with 16-byte st.global.v4 on its aligned body
-// and scalar stores on the (<= 3 element) head/tail.  Values are moved as
-// uint32/uint64 words, so the copy is bit-exact (-0.0, denormals, NaN
-// payloads).  See hprime_plan.h for the index map.
+// Persistent, warp-specialised CTAs.  Producer warp(s) take work units --
+// from a per-launch ticket counter (HP_FLAG_DYNAMIC, the tuned plans) or
+// round-robin u = blockIdx.x + k * gridDim.x -- and stage each unit's n_x
+// source runs with 1-D bulk TMA (cp.async.bulk global -> shared, completion
+// on a full mbarrier) into a ring of `stages` shared-memory buffers.  The
+// consumer warps gather the mirrored, phase-shifted output rows out of
+// shared memory (the row consumer, or the (row, phase-class) task consumer
+// with HP_FLAG_TASKS) and write them with 16-byte st.global.v4 on each row's
+// aligned body and scalar stores on the (<= 3 element) head/tail, then
+// release the stage on an empty mbarrier.  Values are moved as uint32/uint64
+// words, so the copy is bit-exact (-0.0, denormals, NaN payloads).  See
+// hprime_plan.h for the index map and DESIGN.md section 3 for the design.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
