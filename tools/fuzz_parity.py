@@ -25,6 +25,9 @@ def run(cases: int, seed: int, verbose: bool = True) -> list:
     knob_sets = [{}, {"LFBP_STAGE_MAX_KB": "2"}, {"LFBP_STAGES": "1"}, {"LFBP_CONSUMER_WARPS": "1"},
                  {"LFBP_SUBWARP": "2"}, {"LFBP_SUBWARP": "32"}, {"LFBP_STAGE_KB": "1"}, {"LFBP_BAND": "2"},
                  {"LFBP_STAGES": "8", "LFBP_STAGE_KB": "8", "LFBP_CONSUMER_WARPS": "16", "LFBP_SUBWARP": "16"}]
+    if "LFBP_KFLAGS" not in os.environ:   # kernel options of the tuned plans (unless forced from outside)
+        knob_sets += [{"LFBP_KFLAGS": "128"}, {"LFBP_KFLAGS": "136", "LFBP_SUBWARP": "8"}, {"LFBP_KFLAGS": "160"},
+                      {"LFBP_KFLAGS": "200", "LFBP_ZCHUNK_MB": "1"}, {"LFBP_KFLAGS": "32", "LFBP_STAGE_MAX_KB": "2"}]
     keys = sorted({k for ks in knob_sets for k in ks})
     bad = []
     for c in range(cases):
