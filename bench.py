@@ -32,9 +32,9 @@ Rank 0 prints one JSON line:
                cpu_baseline_port: the oracle's numpy restatement on all host
                threads
 ``--impl reference`` prints the same metric for the CPU arm alone: the
-unmodified reference (baseline/_ref) on a bounded plane sample of the same
-config, one process per plane on every host thread (the oracle port when the
-reference is not installed).
+oracle's numpy restatement of the reference on every host thread, on a
+bounded plane sample of the same config (``--ref-mode unmodified``: the
+unmodified reference from baseline/_ref, one process per plane).
 """
 from __future__ import annotations
 
@@ -56,7 +56,7 @@ sys.path.insert(0, ROOT)
 METRIC = "H' build GB/s (bytes read+written)"
 L2_BYTES = 126 << 20
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
-REF_DIR = os.environ.get("LFBP_REF_DIR") or os.path.join(ROOT, "baseline", "_ref")  # the reference install
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # the reference install (side measurements only)
 
 
 def _peaks():
@@ -272,17 +272,22 @@ def run_reference_processes(args, w, procs: int):
 
 
 def run_reference(args, w):
-    """--impl reference: the reference's own CPU path on the box's host cores.
-    With baseline/_ref installed this is the UNMODIFIED lfbp.compute_backprojection
-    (single-threaded numpy as shipped), one process per plane on every host
-    thread; without it, the oracle's numpy restatement on every host thread.
-    Each step is a bounded plane sample of the same workload."""
+    """--impl reference: the reference algorithm on the box's host cores, a
+    bounded plane sample of the same workload per step.  Default (this
+    tier's reference arm): the oracle's numpy restatement of
+    lfbp.compute_backprojection on every host thread -- the reference is
+    Python, so there is no compiled oracle/_ref.  --ref-mode unmodified runs
+    the UNMODIFIED lfbp from baseline/_ref instead (single-threaded numpy as
+    shipped, one process per plane on every host thread), a side
+    measurement."""
     rank, world, _ = _dist()
     if world > 1 and rank != 0:
         return 0
     threads = _threads()
     sample = None
-    if os.path.isdir(os.path.join(REF_DIR, "lfbp")):
+    if args.ref_mode == "unmodified":
+        if not os.path.isdir(os.path.join(REF_DIR, "lfbp")):
+            raise SystemExit("--ref-mode unmodified needs baseline/_ref (tools/install_reference.sh)")
         procs = max(1, min(threads, w.shape[4], args.cpu_planes or threads))
         # bound host memory: ~3 x plane bytes per process (reference peak RSS)
         try:
@@ -313,8 +318,7 @@ def run_reference(args, w):
         nbytes = 2 * H.nbytes
         kind, cores = "port", threads
         what = ("oracle/hprime_oracle.py: numpy restatement of lfbp.compute_backprojection "
-                "(transform.py:113-135), planes and output columns split over host threads "
-                "(baseline/_ref not installed)")
+                "(transform.py:113-135), planes and output columns split over host threads")
         sample = (f"planes [{z0}, {z0 + planes}) of {w.shape[4]} of {w.name} per step (chunked: planes are "
                   f"independent, reference test_transform.py:141-154)")
         extra = {}
@@ -408,6 +412,9 @@ def main():
     ap.add_argument("--weak", action="store_true", help="every rank a full replica instead of the z-split")
     ap.add_argument("--strong", action="store_true", help="(default) z-split of one array over the ranks")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-mode", default="port", choices=["port", "unmodified"],
+                    help="reference arm: the oracle port on every host thread (default), or the unmodified "
+                         "lfbp from baseline/_ref, one process per plane")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-planes", type=int, default=0, help="planes per CPU sample (0: about 1.5 GB)")
     ap.add_argument("--no-cpu", action="store_true")

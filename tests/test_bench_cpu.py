@@ -13,19 +13,18 @@ import pytest
 REF_INSTALLED = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "lfbp"))
 
 
-@pytest.mark.parametrize("arm", ["reference", "port"])
+@pytest.mark.parametrize("arm", ["port", "reference"])
 def test_reference_arm_json_line(arm):
-    """The reference arm: the unmodified lfbp from baseline/_ref, one process
-    per plane (kind "reference", checked against the reference's digests),
-    or the oracle port when the reference is not installed."""
+    """The reference arm: the oracle's numpy restatement on every host thread
+    (default, kind "port"), or with --ref-mode unmodified the unmodified lfbp
+    from baseline/_ref, one process per plane (kind "reference", checked
+    against the reference's digests)."""
     if arm == "reference" and not REF_INSTALLED:
         pytest.skip("baseline/_ref not installed (tools/install_reference.sh)")
-    env = dict(os.environ)
-    if arm == "port":
-        env["LFBP_REF_DIR"] = os.path.join(ROOT, "no-such-dir")
+    extra = ["--ref-mode", "unmodified"] if arm == "reference" else []
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
-                        "--steps", "2", "--warmup", "1", "--cpu-planes", "2"],
-                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+                        "--steps", "2", "--warmup", "1", "--cpu-planes", "2", *extra],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
