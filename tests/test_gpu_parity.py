@@ -94,7 +94,8 @@ def test_inverse_refused_for_even_dims():
 def test_baseline_config_matches_reference_digests(cfg):
     """Full-size BASELINE configs: every plane of the device H' has the SHA-256
     of the reference's H' (computed by lfbp itself, tests/golden/), C5
-    included (71 GB in + 71 GB out resident on one GPU)."""
+    included (71 GB in + 71 GB out resident on one GPU); the inverse of a
+    leading slab of H' returns the input planes' digests."""
     torch = _torch()
     from paper_2003_09133_b200 import f_order_empty, hprime_device
     from paper_2003_09133_b200.configs import WORKLOADS
@@ -121,6 +122,14 @@ def test_baseline_config_matches_reference_digests(cfg):
     got = plane_digests(out, w.shape)
     bad = [z for z in range(w.shape[4]) if got[z] != d["hprime_plane_sha256"][z]]
     assert not bad, f"{cfg}: planes {bad[:8]} differ from the reference"
+    # the inverse (compute_psf_from_backprojection) on a leading slab of H'
+    # (an F-ordered view of its first k planes; a third full C5 array would
+    # not fit next to H and H') returns the input planes
+    k = min(w.shape[4], 16)
+    out_slab = out.permute(4, 3, 2, 1, 0)[:k].permute(4, 3, 2, 1, 0)
+    back = hprime_device(out_slab, inverse=True)
+    torch.cuda.synchronize()
+    assert plane_digests(back, (*w.shape[:4], k)) == d["input_plane_sha256"][:k]
 
 
 @pytest.mark.parametrize("shape,dtype", [
@@ -246,7 +255,7 @@ def test_z_range_writes_only_its_planes():
     assert (got[..., :2] == -7.0).all() and (got[..., 5:] == -7.0).all()
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C4"])
+@pytest.mark.parametrize("cfg", ["C2", "C4", "C3"])
 def test_full_size_involution_on_device(cfg):
     """rearrange(rearrange(H)) == H byte for byte at full BASELINE size
     (odd n_s, n_t: the map is an involution), compared on the device."""
