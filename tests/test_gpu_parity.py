@@ -5,6 +5,7 @@ arrays (tests/golden/small_cases.npz), against the reference's per-plane
 SHA-256 digests for the BASELINE configs (tests/golden/digests_C*.json), and
 against the CPU oracle (oracle/hprime_oracle.py) on seeded inputs.
 """
+import functools
 import os
 
 import numpy as np
@@ -201,6 +202,15 @@ ORDER_SHAPES = [
 ]
 
 
+@functools.lru_cache(maxsize=4)
+def _order_case(shape, dtype):
+    """Input and oracle H' of one unit-order shape, shared by all the plan
+    variants tested on it (the C5-plane shape takes ~10 s on the host)."""
+    from paper_2003_09133_b200.synth import random_psf_like_reference
+    H = random_psf_like_reference(shape, density=0.9, seed=sum(shape) + 3, dtype=dtype)
+    return H, fbytes(hprime_oracle(H))
+
+
 @pytest.mark.parametrize("env", [
     {"LFBP_KFLAGS": "8"}, {"LFBP_KFLAGS": "24"}, {"LFBP_KFLAGS": "8", "LFBP_TILE_Y": "3"},
     {"LFBP_KFLAGS": "16"}, {"LFBP_KFLAGS": "24", "LFBP_STAGE_MAX_KB": "2"},
@@ -229,10 +239,10 @@ def test_unit_orders_are_bit_exact(monkeypatch, env, shape, dtype):
         monkeypatch.setenv(k, v)
     p = plan(shape, dtype)
     assert p["flags"] == int(env["LFBP_KFLAGS"])
-    H = random_psf_like_reference(shape, density=0.9, seed=sum(shape) + 3, dtype=dtype)
+    H, want = _order_case(shape, dtype)
     out = hprime_device(to_device(H))
     torch.cuda.synchronize()
-    assert to_host(out).tobytes() == fbytes(hprime_oracle(H))
+    assert to_host(out).tobytes() == want
     if shape[0] % 2 and shape[1] % 2:
         back = hprime_device(out, inverse=True)
         torch.cuda.synchronize()
