@@ -384,6 +384,53 @@ class HostBuffer:
         _native.lib().lfbp_host_cache_release()
 
 
+class SharedHostOut:
+    """The z-split's one host H' for the e2e leg: a file under /dev/shm that
+    every rank maps (``shard.open_shared_host``); this rank writes its slab
+    [z0, z1) in place, page-locked with cudaHostRegister outside the timed
+    region.  ``ok`` is False (private buffers are used) when /dev/shm cannot
+    hold the array."""
+
+    def __init__(self, w, z0, z1, plane_bytes, rank, world, barrier):
+        import torch
+        self.path = f"/dev/shm/lfbp_bench_{os.environ.get('MASTER_PORT', '0')}_{w.name}.hp"
+        self.rank, self.barrier, self.registered, self.arr, self._mm = rank, barrier, False, None, None
+        free = 0
+        try:
+            st = os.statvfs("/dev/shm")
+            free = st.f_bavail * st.f_frsize
+        except OSError:
+            pass
+        self.ok = all(_gather_objects(free > 1.05 * w.nbytes + (2 << 30), world))
+        if not self.ok:
+            return
+        if rank == 0:
+            with open(self.path, "wb") as f:
+                f.truncate(w.nbytes)
+        barrier()
+        from paper_2003_09133_b200.shard import open_shared_host
+        self._mm = open_shared_host(self.path, (w.nbytes,), np.uint8)
+        self.arr = self._mm[z0 * plane_bytes:z1 * plane_bytes]
+        if self.arr.size:
+            self.arr[::4096] = 0                       # fault the tmpfs pages in, outside the timed region
+            rc = torch.cuda.cudart().cudaHostRegister(self.arr.ctypes.data, self.arr.size, 0)
+            self.registered = int(rc) == 0
+
+    def free(self):
+        import torch
+        if self.registered:
+            torch.cuda.cudart().cudaHostUnregister(self.arr.ctypes.data)
+            self.registered = False
+        self.arr = self._mm = None
+        if self.ok:
+            self.barrier()
+            if self.rank == 0:
+                try:
+                    os.unlink(self.path)
+                except OSError:
+                    pass
+
+
 def _host_plane_digests(buf: np.ndarray, plane_bytes: int, n_planes: int) -> list[str]:
     import concurrent.futures as cf
 
@@ -525,12 +572,18 @@ def main():
             verified = plane_digests(out, shape, threads=min(16, _threads())) == want[z0:z1]
         torch._C._host_emptyCache()   # the digest staging buffers, before the e2e leg pins its own
 
-    # end to end through the C-ABI host path on this rank's whole slab
+    # end to end through the C-ABI host path on this rank's whole slab; under
+    # the z-split every rank writes its slab straight into ONE shared host H'
+    # (a /dev/shm file mapped by every rank, shard.open_shared_host) -- the
+    # final gather of the z-shards, no collective
     e2e = None
+    shared = None
+    if not args.no_e2e and world > 1 and not args.weak and os.environ.get("LFBP_BENCH_SHARED_OUT", "1") != "0":
+        shared = SharedHostOut(w, z0, z1, plane_bytes, rank, world, barrier)
     if not args.no_e2e and nz:
         nbytes = n_elems * w.itemsize
         hin = HostBuffer(nbytes, pinned=True)
-        hout = HostBuffer(nbytes, pinned=hin.pinned)
+        hout = shared if shared is not None and shared.ok else HostBuffer(nbytes, pinned=hin.pinned)
         torch.from_numpy(hin.arr).copy_(src.permute(4, 3, 2, 1, 0).reshape(-1).view(torch.uint8))
         code = _native.F32 if w.itemsize == 4 else _native.F64
         dvec = _native.dims_array(shape)
@@ -561,8 +614,13 @@ def main():
                "host_buffers": "pinned (lfbp_host_alloc)" if hin.pinned else
                                "pageable, staged through pinned chunks (LFBP_HOST_STAGE)",
                "matches_reference_digests": ok, "timing": "wall clock around the synchronous call, max over ranks"}
+        if hout is shared:
+            e2e["host_output"] = (f"one shared host H' ({shared.path}, mapped by every rank; each rank's slab "
+                                  f"page-locked in place: {shared.registered}); digests read back from it")
         hin.free()
         hout.free()
+    elif shared is not None:
+        shared.free()
 
     shard_info = _gather_objects({"rank": rank, "planes": [z0, z1], "kernel_ms_avg": round(statistics.mean(kern_ms), 4)
                                   if kern_ms and nz else 0.0, "verified": verified,

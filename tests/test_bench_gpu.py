@@ -64,3 +64,4 @@ def test_bench_z_split_two_ranks_verifies_every_slab():
     assert all(s["verified"] is True for s in d["shards"]["per_rank"])
     assert d["verified_vs_reference_digests"] is True
     assert d["e2e"]["matches_reference_digests"] is True
+    assert "shared host H'" in d["e2e"].get("host_output", "")   # one host H' gathered from both slabs
